@@ -1,0 +1,213 @@
+/*
+ * deltasnap_cuda.h -- C ABI of the B200 (sm_100a) checkpoint hot path.
+ *
+ * Drop-in boundary for the reference package `deltasnap` (Check-N-Run,
+ * arXiv 2010.08679; /root/reference/pkg/src/deltasnap).  The reference has no
+ * FFI: its boundary is the Python API.  Each entry point below replaces the
+ * numpy body of one reference function, cited as file:line.  The Python
+ * package paper_2010_08679_b200 binds these with ctypes and
+ * keeps the reference names, argument meaning and exceptions.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ *    unless the name ends in _host.  `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).  Calls are asynchronous on
+ *    `stream` and allocate nothing; scratch comes from a caller workspace
+ *    sized by the matching *_workspace_size call.
+ *  - Synchronous argument errors are returned as a ds_status.  Data
+ *    dependent errors (out-of-range ids, NaN/Inf rows, bad padding) are
+ *    OR-ed into a caller-owned device flag word (DS_FLAG_*) that the host
+ *    shim reads at its next synchronisation point and raises as the
+ *    reference exception.
+ *  - Re-entrant: no global mutable state; one stream per caller.
+ *
+ * Bitmaps are uint32 little-endian words, bit r of a table at word r>>5,
+ * bit r&31: byte-identical to the reference's uint8[(rows+7)//8] with bit r
+ * at byte r>>3, bit r&7 (tracker.py:25,36).
+ *
+ * A "table set" is a concatenation of tables inside one word buffer:
+ * table t owns words [word_off[t], word_off[t+1]) and rows [0, rows[t]).
+ */
+#ifndef DELTASNAP_CUDA_H
+#define DELTASNAP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DS_API __attribute__((visibility("default")))
+#else
+#define DS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; 1-6 map 1:1 onto deltasnap/errors.py:4-41. */
+typedef enum {
+    DS_OK = 0,
+    DS_ERR_CONFIG = 1,    /* ConfigError     (errors.py:7-8)   */
+    DS_ERR_DATA = 2,      /* DataError       (errors.py:11-12) */
+    DS_ERR_SHAPE = 3,     /* ShapeError      (errors.py:15-16) */
+    DS_ERR_BOUNDS = 4,    /* BoundsError     (errors.py:19-20) */
+    DS_ERR_FORMAT = 5,    /* FormatError     (errors.py:23-24) */
+    DS_ERR_INTEGRITY = 6, /* IntegrityError  (errors.py:27-28) */
+    DS_ERR_CUDA = 7,      /* CUDA runtime failure (launch/config) */
+    DS_ERR_ARG = 8        /* invalid pointer/size argument        */
+} ds_status;
+
+/* Device flag bits (data-dependent errors, raised at the next sync). */
+#define DS_FLAG_BOUNDS 0x1u    /* mark: id < 0 or >= rows          -> BoundsError    */
+#define DS_FLAG_DATA 0x2u      /* NaN/Inf element in a coded row   -> DataError      */
+#define DS_FLAG_FORMAT 0x4u    /* nonzero padding bits / bad code  -> FormatError    */
+#define DS_FLAG_INTEGRITY 0x8u /* restore row id out of range      -> IntegrityError */
+
+/* Library identity / diagnostics. */
+DS_API const char *ds_version(void);
+DS_API const char *ds_last_error(void); /* thread-local text of the last non-OK status */
+DS_API int ds_device_sm_count(int device);
+
+/* ------------------------------------------------------------------ */
+/* K1 / tracking (tracker.py:27-36, :91-92, :132-134)                   */
+/* ------------------------------------------------------------------ */
+
+/* DirtyBitmap.mark for a table set: idx[i] (int64) belongs to table
+ * seg_table[s] for i in [seg_off[s], seg_off[s+1]).  Test-before-set
+ * atomicOr into words.  Out-of-range ids set DS_FLAG_BOUNDS and are
+ * skipped.  word_off/rows describe the table set (host arrays, at most
+ * 64 tables per call); seg_table == NULL maps every segment to table 0. */
+DS_API int ds_mark(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+            const int64_t *idx, const int64_t *seg_off_host, const int32_t *seg_table_host,
+            int nseg, uint32_t *flags, void *stream);
+
+/* Single-table convenience form (DirtyBitmap.mark). */
+DS_API int ds_mark_table(uint32_t *words, int64_t rows, const int64_t *idx, int64_t n, uint32_t *flags,
+                  void *stream);
+
+/* ------------------------------------------------------------------ */
+/* K0 / bitmap maintenance (tracker.py:38-61, :120-130)                 */
+/* ------------------------------------------------------------------ */
+
+/* op 0: dst = a | b (merge_or); op 1: dst |= a (merge_in);
+ * op 2: b |= a; a = 0 (reset_interval fold); op 3: a = 0; b = 0 (reset_baseline). */
+DS_API int ds_bitmap_op(uint32_t *dst, uint32_t *a, uint32_t *b, int64_t nwords, int op, void *stream);
+
+/* popcount of nwords words into *out (device int64). */
+DS_API int ds_popcount(const uint32_t *words, int64_t nwords, int64_t *out, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* K2 / compaction (tracker.py:54-58, :100-124)                          */
+/* ------------------------------------------------------------------ */
+
+/* Capture both scopes of a tracker in one pass.
+ *   interval, baseline: table-set word buffers (same layout);
+ *   word_off[ntables+1] and rows[ntables] (device);
+ *   ids_int / ids_union: outputs (int64 row ids, per table ascending,
+ *     tables concatenated in order), either may be NULL to skip a scope;
+ *   counts[2*ntables+2] (device int64): counts[t] interval count of table t,
+ *     counts[ntables+1+t] union count; counts[ntables] and counts[2*ntables+1]
+ *     the totals;  offsets follow as exclusive prefix sums on the host side.
+ *   fold: 0 none, 1 reset_interval (baseline |= interval; interval = 0)
+ *     after reading, 2 reset_baseline (both cleared).
+ * Workspace: ds_capture_workspace_size(total_words). */
+DS_API size_t ds_capture_workspace_size(int64_t total_words, int ntables);
+DS_API int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t *word_off_host,
+               const int64_t *rows_host, int ntables, int64_t *ids_int, int64_t *ids_union,
+               int64_t *counts, int fold, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* K3 / writer (engine.py:118-189, quant.py:93-209,372-382,             */
+/*              payload.py:68-104)                                       */
+/* ------------------------------------------------------------------ */
+
+/* One table of a shard payload, as seen by the writer. */
+typedef struct {
+    const float *values;  /* (rows, ld) float32, device */
+    const float *aux;     /* (rows, ld) float32 or NULL */
+    int64_t ld;           /* row stride in elements (>= dim) */
+    int64_t rows;         /* table rows (full checkpoints write all of them) */
+    int64_t row_base;     /* global id of local row 0 (row-sharded tables) */
+    int64_t ids_off;      /* offset of this table's ids in the id buffer (incremental) */
+    uint32_t table_id;
+    uint32_t dim;
+} ds_table_desc;
+
+/* Shard-level parameters of a checkpoint. */
+typedef struct {
+    int bitwidth;       /* 2,3,4,8; 0 = fp32 section (mode 0, tag 32) */
+    int incremental;    /* 1: records carry u64 row ids, rows from ids */
+    int adaptive_bins;  /* 0: naive min/max ranges; else greedy num_bins */
+    int adaptive_steps; /* floor(num_bins*ratio + 1e-9) (quant.py:186) */
+    int write_headers;  /* 1: write the 24-byte CNR1 section headers */
+    int aux;            /* 1: aux_flag set, aux rows appended (payload.py:102-103) */
+    unsigned long long *stats; /* optional device counters (DS_STAT_*), may be NULL */
+} ds_ckpt_params;
+
+/* Counters of the certified fast path (diagnostics). */
+#define DS_STAT_EXACT_DECISIONS 0 /* greedy comparisons re-decided in exact f64 */
+#define DS_STAT_EXACT_CODES 1     /* element codes recomputed in exact f64      */
+#define DS_STAT_ROWS 2            /* rows coded                                 */
+#define DS_STAT_COUNT 4
+
+/* Payload layout for ntables tables: given per-table row counts (device,
+ * counts[t]; full checkpoints pass NULL and use rows), computes on device
+ *   sec_off[t]   byte offset of table t's section (header) in the payload,
+ *   sec_off[ntables] total payload bytes,
+ * and the tile schedule the writer uses.  Everything stays on device. */
+DS_API size_t ds_writer_workspace_size(int ntables, int64_t max_rows);
+DS_API int ds_write_payload(const ds_table_desc *tables_host, int ntables, const ds_ckpt_params *p,
+                     const int64_t *ids, const int64_t *counts, uint8_t *payload,
+                     int64_t payload_capacity, int64_t *sec_off, double *err_sum,
+                     uint32_t *flags, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Upper bound of the payload bytes for the given row counts (host math). */
+DS_API int64_t ds_record_size(int64_t dim, int bitwidth, int aux, int incremental);
+
+/* ------------------------------------------------------------------ */
+/* K4 / restore (engine.py:459-485, payload.py:60-65, quant.py:385-395) */
+/* ------------------------------------------------------------------ */
+
+/* Apply one section body (records only, header parsed on the host) to a
+ * (local) table holding global rows [row_lo, row_hi):
+ *   incremental: record row ids; ids outside [0, table_rows) set
+ *     DS_FLAG_INTEGRITY; ids outside [row_lo, row_hi) are skipped (other
+ *     rank's rows); applied rows also set their since-baseline bit
+ *     (engine.py:476) in baseline_words (may be NULL);
+ *   full: record i is global row i; only [row_lo, row_hi) is applied.
+ * Nonzero padding bits set DS_FLAG_FORMAT. */
+DS_API int ds_restore_section(const uint8_t *body, int64_t nrec, int64_t dim, int bitwidth, int aux,
+                       int incremental, int64_t table_rows, int64_t row_lo, int64_t row_hi,
+                       float *values, int64_t ld, float *aux_values, uint32_t *baseline_words,
+                       uint32_t *flags, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Row-matrix codec entry points (quant.py API mirror)                  */
+/* ------------------------------------------------------------------ */
+
+/* quantize_rows (quant.py:93-106): codes[n,d] from x[n,d] and f32 ranges. */
+DS_API int ds_quantize_rows(const float *x, int64_t n, int64_t d, const float *mins, const float *maxs,
+                     int bitwidth, uint8_t *codes, void *stream);
+/* dequantize_rows (quant.py:109-115); codes >= 2^N set DS_FLAG_FORMAT. */
+DS_API int ds_dequantize_rows(const uint8_t *codes, int64_t n, int64_t d, const float *mins,
+                       const float *maxs, int bitwidth, float *out, uint32_t *flags,
+                       void *stream);
+/* reconstruction_errors (quant.py:134-138), exact numpy order, f64 out. */
+DS_API int ds_reconstruction_errors(const float *x, int64_t n, int64_t d, const float *mins,
+                             const float *maxs, int bitwidth, double *out, void *stream);
+/* adaptive_params_rows (quant.py:160-209): greedy ranges (NaN/Inf flag). */
+DS_API int ds_adaptive_params_rows(const float *x, int64_t n, int64_t d, int bitwidth, int num_bins,
+                            int steps, float *mins, float *maxs, uint32_t *flags,
+                            unsigned long long *stats, void *stream);
+/* naive x.min(axis=1) / x.max(axis=1). */
+DS_API int ds_row_minmax(const float *x, int64_t n, int64_t d, float *mins, float *maxs, void *stream);
+/* pack_code_rows / unpack_code_rows (quant.py:376-395). */
+DS_API int ds_pack_code_rows(const uint8_t *codes, int64_t n, int64_t d, int bitwidth, uint8_t *out,
+                      uint32_t *flags, void *stream);
+DS_API int ds_unpack_code_rows(const uint8_t *packed, int64_t n, int64_t d, int bitwidth, uint8_t *out,
+                        uint32_t *flags, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTASNAP_CUDA_H */

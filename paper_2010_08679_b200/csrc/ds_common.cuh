@@ -1,0 +1,431 @@
+// ds_common.cuh -- shared device code of the sm_100a checkpoint hot path.
+//
+// Row-group model: one embedding row is owned by a group of G lanes
+// (G = 1..32, a power of two, groups aligned inside a warp).  Lane `lig` of
+// the group holds EPL = VEC*C elements in registers:
+//   VEC == 4 : chunk c holds elements 4*(lig + c*G) .. +3   (one 128-bit load)
+//   VEC == 1 : element k is lig + k*G                         (scalar loads)
+//
+// Numerics (quant.py:89-138):
+//   * "exact" helpers reproduce the reference float64 arithmetic bit for bit
+//     with explicit __d*_rn intrinsics (never contracted into FMA);
+//   * "fast" helpers run in fp32 and return a certified error bound; a
+//     decision whose margin is below the bound is re-taken exactly.  Only the
+//     decisions feed the output, so the output equals the exact one.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/deltasnap_cuda.h"
+
+#define DS_FULL_MASK 0xffffffffu
+#define DS_MAX_TABLES 64
+#define DS_HEADER_SIZE 24
+#define DS_FP32_TAG 32
+
+namespace ds {
+
+constexpr float kU = 5.9604644775390625e-08f;  // 2^-24, unit roundoff of fp32
+
+// ---------------------------------------------------------------------------
+// group reductions (width G shuffles; every lane of the warp participates)
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ float grp_min(float v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(DS_FULL_MASK, v, o, G));
+    return v;
+}
+template <int G>
+__device__ __forceinline__ float grp_max(float v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(DS_FULL_MASK, v, o, G));
+    return v;
+}
+template <int G>
+__device__ __forceinline__ float grp_sum(float v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(DS_FULL_MASK, v, o, G);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ double grp_sumd(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(DS_FULL_MASK, v, o, G);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int grp_or(int v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(DS_FULL_MASK, v, o, G);
+    return v;
+}
+
+template <int G>
+constexpr int log2i() { return G <= 1 ? 0 : 1 + log2i<G / 2>(); }
+
+// ---------------------------------------------------------------------------
+// element layout
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC>
+struct Layout {
+    static constexpr int EPL = C * VEC;
+    __device__ __forceinline__ static int elem(int lig, int k) {
+        if (VEC == 4) return 4 * (lig + (k >> 2) * G) + (k & 3);
+        return lig + k * G;
+    }
+};
+
+// Load one row (values + row*ld) into registers; padding elements get `pad`.
+template <int G, int C, int VEC>
+__device__ __forceinline__ void load_row(const float *__restrict__ row, int d, int lig,
+                                         float (&x)[C * VEC], float pad) {
+    if (VEC == 4) {
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            int e = 4 * (lig + c * G);
+            if (e < d) {
+                float4 v = __ldg(reinterpret_cast<const float4 *>(row + e));
+                x[4 * c + 0] = v.x;
+                x[4 * c + 1] = v.y;
+                x[4 * c + 2] = v.z;
+                x[4 * c + 3] = v.w;
+            } else {
+                x[4 * c + 0] = x[4 * c + 1] = x[4 * c + 2] = x[4 * c + 3] = pad;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < C; k++) {
+            int e = lig + k * G;
+            x[k] = e < d ? __ldg(row + e) : pad;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact reference arithmetic (quant.py:89-115)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double scale64(float lo, float hi, int L) {
+    return __ddiv_rn(__dsub_rn((double)hi, (double)lo), (double)L);  // _scales :89-90
+}
+
+// quantize_rows element: clip (PyArray_MAX/MIN), true f64 division,
+// floor(v + 0.5), clip to [0, L] (quant.py:99-106).
+__device__ __forceinline__ int code_exact(float x, float lo, float hi, double s, int L) {
+    double safe = s > 0.0 ? s : 1.0;
+    float c = x > lo ? x : lo;
+    c = c < hi ? c : hi;
+    double v = __ddiv_rn(__dsub_rn((double)c, (double)lo), safe);
+    double q = floor(__dadd_rn(v, 0.5));
+    q = q < 0.0 ? 0.0 : q;
+    q = q > (double)L ? (double)L : q;
+    return (int)q;
+}
+
+// dequantize_rows element: two rounded f64 ops, then f32 (quant.py:114-115).
+__device__ __forceinline__ float deq_exact(int q, float lo, double s) {
+    return __double2float_rn(__dadd_rn(__dmul_rn(s, (double)q), (double)lo));
+}
+
+// ---------------------------------------------------------------------------
+// final codes of a row with fixed (lo, hi): fp32 guard band + exact fallback
+// ---------------------------------------------------------------------------
+struct RowQ {
+    float lo, hi, inv, eps;
+    double s;
+    int L;
+    int mode;  // 0 fast, 1 all-zero (degenerate range), 2 exact every element
+};
+
+__device__ __forceinline__ RowQ make_rowq(float lo, float hi, int L) {
+    RowQ r;
+    r.lo = lo;
+    r.hi = hi;
+    r.L = L;
+    r.s = scale64(lo, hi, L);
+    float rng = __fsub_rn(hi, lo);
+    r.inv = 0.f;
+    r.eps = 0.f;
+    if (!(r.s > 0.0)) {
+        r.mode = 1;  // scale 0 -> safe 1 -> v = 0 -> code 0 (quant.py:101-106)
+    } else if (!(rng >= 1e-30f && rng <= 1e30f && fabsf(lo) <= 1e30f && fabsf(hi) <= 1e30f)) {
+        r.mode = 2;
+    } else {
+        r.mode = 0;
+        r.inv = __fdiv_rn((float)L, rng);
+        // |v_fast - v_ref| <= 5u*L (c-lo, rng, div, mul roundings); 8u*L margin
+        r.eps = 8.f * kU * (float)L;
+    }
+    return r;
+}
+
+// Returns the reference code of x.  `nexact` counts exact recomputations.
+__device__ __forceinline__ int code_of(float x, const RowQ &r, unsigned &nexact) {
+    if (r.mode == 1) return 0;
+    if (r.mode == 0) {
+        float c = fminf(fmaxf(x, r.lo), r.hi);
+        float v = __fmul_rn(__fsub_rn(c, r.lo), r.inv);
+        float q = rintf(v);
+        if (fabsf(__fsub_rn(v, q)) <= 0.5f - r.eps) return (int)q;
+    }
+    nexact++;
+    return code_exact(x, r.lo, r.hi, r.s, r.L);
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise summation on shared memory (loops_utils.h.src; the order of
+// np.linalg.norm at quant.py:138).  Single-thread forms.
+// ---------------------------------------------------------------------------
+static __device__ double pw_block(const double *a, int n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+static __device__ double pw_sum(const double *a, int n) {
+    // explicit stack instead of recursion: leaves of <= 128 elements combined
+    // in the same binary-tree order numpy's recursion uses.
+    if (n <= 128) return pw_block(a, n);
+    struct Frame {
+        int off, n, state;
+        double left;
+    };
+    Frame st[24];
+    int sp = 0;
+    st[0] = {0, n, 0, 0.0};
+    double ret = 0.0;
+    while (true) {
+        Frame &f = st[sp];
+        if (f.n <= 128) {
+            ret = pw_block(a + f.off, f.n);
+            if (sp == 0) return ret;
+            sp--;
+            continue;
+        }
+        int n2 = f.n / 2;
+        n2 -= n2 % 8;
+        if (f.state == 0) {  // descend left
+            f.state = 1;
+            st[sp + 1] = {f.off, n2, 0, 0.0};
+            sp++;
+        } else if (f.state == 1) {  // left done -> descend right
+            f.left = ret;
+            f.state = 2;
+            st[sp + 1] = {f.off + n2, f.n - n2, 0, 0.0};
+            sp++;
+        } else {  // both done
+            ret = __dadd_rn(f.left, ret);
+            if (sp == 0) return ret;
+            sp--;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// exact ME of one candidate for every group of a warp (warp-collective).
+// `buf` points at this group's scratch of >= d doubles (+8 for r[]).
+// Lanes whose group has want == false still take part in the syncs.
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC>
+__device__ __noinline__ double exact_me_group(const float (&x)[C * VEC], int d, int lig,
+                                              float lo, float hi, int L, bool want,
+                                              double *buf, unsigned &nexact_codes) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    if (want) {
+        RowQ rq = make_rowq(lo, hi, L);
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            int e = Lay::elem(lig, k);
+            if (e < d) {
+                int q = code_of(x[k], rq, nexact_codes);
+                float dq = deq_exact(q, lo, rq.s);
+                double err = __dsub_rn((double)x[k], (double)dq);
+                buf[e] = __dmul_rn(err, err);
+            }
+        }
+    }
+    __syncwarp();
+    double res = 0.0;
+    if (d <= 128 && d >= 8) {
+        // accumulator j (< 8) handled by lane j % G of the group
+        if (want) {
+            for (int j = lig; j < 8; j += G) {
+                double r = buf[j];
+                for (int i = 8; i < d - (d % 8); i += 8) r = __dadd_rn(r, buf[i + j]);
+                buf[d + j] = r;
+            }
+        }
+        __syncwarp();
+        if (want && lig == 0) {
+            const double *r = buf + d;
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (int i = d - (d % 8); i < d; i++) res = __dadd_rn(res, buf[i]);
+        }
+    } else {
+        if (want && lig == 0) res = pw_sum(buf, d);
+        __syncwarp();
+    }
+    __syncwarp();
+    // broadcast from the group leader
+    int lane = threadIdx.x & 31;
+    res = __shfl_sync(DS_FULL_MASK, res, lane & ~(G - 1));
+    return __dsqrt_rn(res);
+}
+
+// ---------------------------------------------------------------------------
+// certified fast ME^2 of one candidate (fp32), see DESIGN.md "numerics".
+// Returns S (sum of squares, fp32 accumulation) and B with |S - S_ref| <= B,
+// where S_ref is the reference's float64 sum for the same candidate.
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC, bool PAD>
+__device__ __forceinline__ void eval_fast(const float (&x)[C * VEC], int d, int lig, float lo,
+                                          float hi, int L, float &S, float &B) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    float rng = __fsub_rn(hi, lo);
+    float M = fmaxf(fabsf(lo), fabsf(hi));
+    bool ok = rng >= 1e-30f && rng <= 1e30f && M <= 1e30f;
+    float inv = ok ? __fdividef((float)L, rng) : 0.f;
+    float s32 = __fmul_rn(rng, 1.0f / (float)L);
+    float sse = 0.f, rmax = 0.f;
+#pragma unroll
+    for (int k = 0; k < EPL; k++) {
+        float c = fminf(fmaxf(x[k], lo), hi);
+        float v = __fmul_rn(__fsub_rn(c, lo), inv);
+        float q = rintf(v);
+        rmax = fmaxf(rmax, fabsf(__fsub_rn(v, q)));
+        float dq = __fmaf_rn(q, s32, lo);
+        float e = __fsub_rn(x[k], dq);
+        if (PAD) e = Lay::elem(lig, k) < d ? e : 0.f;
+        sse = __fmaf_rn(e, e, sse);
+    }
+    S = grp_sum<G>(sse);
+    rmax = grp_max<G>(rmax);
+    if (!ok) {
+        B = INFINITY;
+        return;
+    }
+    float fd = (float)d;
+    float delta = 16.f * kU * M + 1e-44f;                // |deq_fast - deq_ref|
+    float epsw = 10.f * kU * (float)L;                   // |v_fast - v_ref|
+    float b = 2.f * delta * sqrtf(fd * S) + 2.f * fd * delta * delta +
+              (float)(EPL + log2i<G>() + 4) * kU * S;
+    if (rmax > 0.5f - epsw) b += fd * 4.f * s32 * (epsw * s32 + 2.f * delta);  // code ties
+    B = 1.5f * b + 1e-37f;
+}
+
+// ---------------------------------------------------------------------------
+// greedy range search of one row per group (quant.py:160-209), certified.
+// All lanes of the warp must call it (exact re-evaluation is warp-collective).
+// ---------------------------------------------------------------------------
+struct Cand {
+    float lo, hi, S, B;
+    double me;    // exact ME when has_me
+    bool has_me;
+};
+
+template <int G, int C, int VEC, bool PAD>
+__device__ __forceinline__ void greedy_row(const float (&x)[C * VEC], int d, int lig, bool row_ok,
+                                           float lo0, float hi0, int L, int bins, int steps,
+                                           double *buf, float &out_lo, float &out_hi,
+                                           unsigned &n_exact_dec, unsigned &n_exact_codes) {
+    double full = __dsub_rn((double)hi0, (double)lo0);
+    double step = __ddiv_rn(full, (double)bins);
+    Cand best;
+    best.lo = lo0;
+    best.hi = hi0;
+    best.has_me = false;
+    best.me = 0.0;
+    eval_fast<G, C, VEC, PAD>(x, d, lig, lo0, hi0, L, best.S, best.B);
+    double cur_lo = (double)lo0, cur_hi = (double)hi0;
+    bool active = row_ok && step > 0.0;
+    for (int it = 0; it < steps; it++) {
+        active = active && (__dsub_rn(__dsub_rn(cur_hi, cur_lo), step) > 0.0);
+        if (!__any_sync(DS_FULL_MASK, active)) break;
+        Cand a, b;
+        a.lo = __double2float_rn(__dadd_rn(cur_lo, step));
+        a.hi = __double2float_rn(cur_hi);
+        b.lo = __double2float_rn(cur_lo);
+        b.hi = __double2float_rn(__dsub_rn(cur_hi, step));
+        a.has_me = b.has_me = false;
+        a.me = b.me = 0.0;
+        eval_fast<G, C, VEC, PAD>(x, d, lig, a.lo, a.hi, L, a.S, a.B);
+        eval_fast<G, C, VEC, PAD>(x, d, lig, b.lo, b.hi, L, b.S, b.B);
+        // take_a = me_a <= me_b (quant.py:198)
+        bool take_a = true;
+        bool sure = true;
+        if (a.S + a.B < b.S - b.B) take_a = true;
+        else if (a.S - a.B > b.S + b.B) take_a = false;
+        else sure = false;
+        bool need = active && !sure;
+        if (__any_sync(DS_FULL_MASK, need)) {
+            double ma = exact_me_group<G, C, VEC>(x, d, lig, a.lo, a.hi, L, need, buf,
+                                                  n_exact_codes);
+            double mb = exact_me_group<G, C, VEC>(x, d, lig, b.lo, b.hi, L, need, buf,
+                                                  n_exact_codes);
+            if (need) {
+                a.me = ma;
+                b.me = mb;
+                a.has_me = b.has_me = true;
+                take_a = ma <= mb;
+                if (lig == 0) n_exact_dec++;
+            }
+        }
+        // no `continue` for inactive rows: the exact paths below are
+        // warp-collective, so every lane walks the same control flow.
+        if (active) {
+            if (take_a) cur_lo = __dadd_rn(cur_lo, step);
+            else cur_hi = __dsub_rn(cur_hi, step);
+        }
+        Cand c = take_a ? a : b;
+        // improved = active & (me_cur < best_me) (quant.py:204)
+        bool improved = false;
+        sure = true;
+        if (!active) improved = false;
+        else if (c.has_me && best.has_me) improved = c.me < best.me;
+        else if (c.S + c.B < best.S - best.B) improved = true;
+        else if (c.S - c.B > best.S + best.B) improved = false;
+        else sure = false;
+        need = !sure;
+        // exact evaluation of whichever side lacks an exact value
+        bool need_c = need && !c.has_me, need_b = need && !best.has_me;
+        if (__any_sync(DS_FULL_MASK, need_c)) {
+            double m = exact_me_group<G, C, VEC>(x, d, lig, c.lo, c.hi, L, need_c, buf,
+                                                 n_exact_codes);
+            if (need_c) { c.me = m; c.has_me = true; }
+        }
+        if (__any_sync(DS_FULL_MASK, need_b)) {
+            double m = exact_me_group<G, C, VEC>(x, d, lig, best.lo, best.hi, L, need_b, buf,
+                                                 n_exact_codes);
+            if (need_b) { best.me = m; best.has_me = true; }
+        }
+        if (need) {
+            improved = c.me < best.me;
+            if (lig == 0) n_exact_dec++;
+        }
+        if (improved) best = c;
+    }
+    out_lo = best.lo;
+    out_hi = best.hi;
+}
+
+}  // namespace ds

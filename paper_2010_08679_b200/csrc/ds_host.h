@@ -1,0 +1,46 @@
+// ds_host.h -- host-side helpers of the C ABI (status text, launch checks, grid sizing).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/deltasnap_cuda.h"
+
+namespace ds {
+namespace host {
+
+// Thread-local text of the last failure (ds_last_error); no shared state.
+inline char *err_buf() {
+    static thread_local char buf[512];
+    return buf;
+}
+
+inline int fail(int status, const char *msg) {
+    snprintf(err_buf(), 512, "%s", msg);
+    return status;
+}
+
+inline int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(err_buf(), 512, "%s: %s", what, cudaGetErrorString(e));
+        return DS_ERR_CUDA;
+    }
+    return DS_OK;
+}
+
+// SM count of the current device, cached per device (read-only after init).
+int sm_count();
+
+// Grid for a grid-stride kernel: enough blocks to cover n, capped at
+// `per_sm` resident blocks per SM.
+inline int64_t grid_for(int64_t n, int threads, int per_sm) {
+    int64_t need = (n + threads - 1) / threads;
+    int64_t cap = (int64_t)sm_count() * per_sm;
+    if (need < 1) need = 1;
+    return need < cap ? need : cap;
+}
+
+}  // namespace host
+}  // namespace ds

@@ -1,0 +1,377 @@
+"""Checkpoint writer and restore on the GPU (the engine.py hot-path mirror).
+
+* build_shard_payload: drop-in for deltasnap/engine.py:118-189.  Same
+  arguments and return value (payload bytes, quantized row count, summed row
+  L2 error); the whole chunk loop runs in one writer launch (ds_writer.cu).
+* ShardWriter: the device-resident form the training loop uses -- tables,
+  ids and counts stay in HBM, nothing synchronises until the payload is
+  copied to pinned host memory.
+* apply_payload / restore_chain / restore: the _restore_at scatter
+  (engine.py:443-512) on device tables (ds_restore.cu); chain/manifest logic
+  stays on the host.
+
+Differences from the reference, all on inputs the reference mishandles:
+NaN/Inf rows raise DataError in every quantized mode (the reference's naive
+8-bit path casts NaN codes silently); negative plan row ids raise BoundsError
+(numpy would wrap them); err_sum agrees with the reference to ~1e-15 relative
+(its float64 sum order depends on chunk_rows, engine.py:171-173).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import device_of, to_device
+from .errors import ConfigError, IntegrityError, ShapeError
+from .payload import HEADER_SIZE, parse_headers, record_size
+from .quant import VALID_BITWIDTHS, AdaptiveConfig, default_adaptive_config
+
+FULL = "full"
+INCREMENTAL = "incremental"
+
+
+@dataclass
+class DeviceTable:
+    """An embedding table (or a row shard of one) resident in HBM.
+
+    values: (rows, dim) float32 CUDA tensor; row_base is the global id of
+    local row 0; total_rows the global row count of the table.
+    """
+
+    table_id: int
+    values: torch.Tensor
+    aux: torch.Tensor | None = None
+    row_base: int = 0
+    total_rows: int | None = None
+
+    def __post_init__(self):
+        if self.total_rows is None:
+            self.total_rows = self.row_base + self.values.shape[0]
+
+    @property
+    def rows(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def dim(self) -> int:
+        return self.values.shape[1]
+
+
+def adaptive_for(bitwidth: int, overrides) -> AdaptiveConfig | None:
+    """engine.py:112-115"""
+    if overrides and bitwidth in overrides:
+        return overrides[bitwidth]
+    return default_adaptive_config(bitwidth)
+
+
+def _as_device_table(t, device) -> DeviceTable:
+    if isinstance(t, DeviceTable):
+        return t
+    values = to_device(t.values, torch.float32, device)
+    aux = None if getattr(t, "aux", None) is None else to_device(t.aux, torch.float32, device)
+    return DeviceTable(int(t.table_id), values, aux)
+
+
+class ShardWriter:
+    """K3 for a fixed set of device tables sharing one dim (<= 64 per launch).
+
+    write() is asynchronous on the current stream; finish() synchronises,
+    raises flagged data errors and returns (payload_bytes, err_sum).
+    """
+
+    def __init__(self, tables: list, bitwidth: int | None, *, adaptive: AdaptiveConfig | None = None,
+                 aux: bool | None = None, write_headers: bool = True, device=None,
+                 stats: torch.Tensor | None = None):
+        if not tables:
+            raise ValueError("ShardWriter needs at least one table")
+        if len(tables) > _lib.MAX_TABLES:
+            raise ValueError("at most 64 tables per ShardWriter; split the shard")
+        if bitwidth is not None and bitwidth not in VALID_BITWIDTHS:
+            raise ConfigError(f"unsupported bitwidth {bitwidth}")
+        self.device = device_of(device if device is not None else tables[0].values.device)
+        self.tables = tables
+        dims = {t.dim for t in tables}
+        if len(dims) != 1:
+            raise ShapeError("tables of one ShardWriter must share dim")
+        self.dim = dims.pop()
+        self.bitwidth = bitwidth
+        self.aux = all(t.aux is not None for t in tables) if aux is None else aux
+        self.adaptive = adaptive if bitwidth is not None else None
+        self.L = _lib.lib()
+        descs = (_lib.TableDesc * len(tables))()
+        for k, t in enumerate(tables):
+            if t.values.dtype != torch.float32 or not t.values.is_cuda:
+                raise ValueError("DeviceTable.values must be a float32 CUDA tensor")
+            if t.values.stride(1) != 1:
+                raise ValueError("DeviceTable.values rows must be contiguous")
+            descs[k].values = t.values.data_ptr()
+            descs[k].aux = t.aux.data_ptr() if (self.aux and t.aux is not None) else None
+            descs[k].ld = t.values.stride(0)
+            descs[k].rows = t.rows
+            descs[k].row_base = t.row_base
+            descs[k].ids_off = 0
+            descs[k].table_id = t.table_id
+            descs[k].dim = t.dim
+        self._descs = descs
+        self.params = _lib.CkptParams()
+        self.params.bitwidth = bitwidth or 0
+        self.params.adaptive_bins = self.adaptive.num_bins if self.adaptive else 0
+        self.params.adaptive_steps = self.adaptive.steps if self.adaptive else 0
+        self.params.write_headers = int(write_headers)
+        self.params.aux = int(self.aux)
+        self.params.stats = None if stats is None else stats.data_ptr()
+        self.write_headers = write_headers
+        ws = int(self.L.ds_writer_workspace_size(len(tables), 0))
+        self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        self.sec_off = torch.zeros(len(tables) + 1, dtype=torch.int64, device=self.device)
+        self.err = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def record_size(self, incremental: bool) -> int:
+        return record_size(self.dim, 1 if self.bitwidth else 0, self.bitwidth, self.aux,
+                           incremental)
+
+    def payload_bytes(self, counts) -> int:
+        rec = self.record_size(counts is not None)
+        rows = counts if counts is not None else [t.rows for t in self.tables]
+        hdr = HEADER_SIZE if self.write_headers else 0
+        return int(sum(hdr + int(n) * rec for n in rows))
+
+    def write(self, payload: torch.Tensor, ids: torch.Tensor | None = None,
+              counts: torch.Tensor | None = None, ids_offsets=None, stream=None) -> None:
+        """Launch layout + writer (+ error reduction).
+
+        Incremental when `ids` is given: ids is the concatenation of every
+        table's global row ids (ascending per table), counts a device int64
+        tensor of per-table lengths, ids_offsets the host start of each
+        table's ids (defaults to the exclusive prefix of the concatenation,
+        which is the layout capture() produces).
+        """
+        incremental = ids is not None
+        self.params.incremental = int(incremental)
+        if incremental:
+            if ids_offsets is None:
+                raise ValueError("ids_offsets required for incremental writes")
+            for k in range(len(self.tables)):
+                self._descs[k].ids_off = int(ids_offsets[k])
+        self.flags.zero_()
+        _lib.check(self.L.ds_write_payload(
+            ctypes.cast(self._descs, ctypes.c_void_p), len(self.tables), ctypes.byref(self.params),
+            ids.data_ptr() if incremental else None,
+            counts.data_ptr() if incremental else None, payload.data_ptr(), payload.numel(),
+            self.sec_off.data_ptr(), self.err.data_ptr(), self.flags.data_ptr(),
+            self._ws.data_ptr(), self._ws.numel(), _lib.stream_handle(stream)), "write_payload")
+
+    def finish(self) -> tuple:
+        """Synchronise; raise flagged errors; (total payload bytes, err_sum)."""
+        flags = int(self.flags.item())
+        _lib.raise_flags(flags, "build_shard_payload")
+        total = int(self.sec_off[-1].item())
+        return total, float(self.err.item())
+
+
+def _group_tables(tables: list) -> list:
+    """Consecutive runs of <= 64 tables sharing a dim (sections stay in order)."""
+    groups, cur = [], []
+    for t in tables:
+        if cur and (t.dim != cur[0].dim or len(cur) == _lib.MAX_TABLES):
+            groups.append(cur)
+            cur = []
+        cur.append(t)
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def build_shard_payload(snap, plan, shard_id: int, chunk_rows: int = 1024,
+                        adaptive_overrides: dict | None = None, *, device=None) -> tuple:
+    """Serialize one shard of a snapshot under a plan (engine.py:118-189).
+
+    snap: anything with shard_tables(shard_id) returning tables with
+    table_id/values/aux (the reference's ModelSnapshot, or DeviceTable lists);
+    host arrays are uploaded, CUDA tensors used in place.  chunk_rows only
+    changes the reference's float64 summation order of err_sum; the bytes do
+    not depend on it (tests/test_engine.py:123-143 upstream).
+    """
+    del chunk_rows
+    dev = device_of(device)
+    incremental = plan.kind == INCREMENTAL
+    bitwidth = plan.bitwidth
+    acfg = adaptive_for(bitwidth, adaptive_overrides) if bitwidth is not None else None
+    tables = [_as_device_table(t, dev) for t in snap.shard_tables(shard_id)]
+    if not tables:
+        return b"", 0, 0.0
+    parts = []
+    q_rows = 0
+    err_sum = 0.0
+    for group in _group_tables(tables):
+        writer = ShardWriter(group, bitwidth, adaptive=acfg, device=dev)
+        if incremental:
+            sels = []
+            for t in group:
+                sel = plan.rows.get(t.table_id)
+                sels.append(to_device(np.zeros(0, np.int64) if sel is None else sel, torch.int64,
+                                      dev).reshape(-1))
+            counts_h = [int(s.numel()) for s in sels]
+            offs = np.concatenate([[0], np.cumsum(counts_h)]).astype(np.int64)
+            ids = torch.cat(sels) if sum(counts_h) else torch.zeros(1, dtype=torch.int64,
+                                                                    device=dev)
+            counts = torch.tensor(counts_h, dtype=torch.int64, device=dev)
+            nbytes = writer.payload_bytes(counts_h)
+            payload = torch.empty(nbytes + 16, dtype=torch.uint8, device=dev)
+            writer.write(payload, ids, counts, offs[:-1])
+            n_rows = sum(counts_h)
+        else:
+            nbytes = writer.payload_bytes(None)
+            payload = torch.empty(nbytes + 16, dtype=torch.uint8, device=dev)
+            writer.write(payload)
+            n_rows = sum(t.rows for t in group)
+        total, err = writer.finish()
+        assert total == nbytes, (total, nbytes)
+        parts.append(payload[:total].cpu().numpy().tobytes())
+        if bitwidth is not None:
+            q_rows += n_rows
+            err_sum += err
+    return b"".join(parts), q_rows, err_sum
+
+
+# ---------------------------------------------------------------------------
+# restore (engine.py:443-535)
+# ---------------------------------------------------------------------------
+
+def _upload_payload(data, dev) -> torch.Tensor:
+    buf = np.frombuffer(data, dtype=np.uint8)
+    out = torch.empty(buf.size + 16, dtype=torch.uint8, device=dev)
+    if buf.size:
+        host = torch.from_numpy(buf.copy()).pin_memory()
+        out[:buf.size].copy_(host, non_blocking=True)
+    return out
+
+
+def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None = None,
+                  device=None) -> None:
+    """Apply one shard payload to device tables (the loop body of
+    engine.py:625-649).
+
+    tables: {table_id: DeviceTable} (row shards allowed: only rows in
+    [row_base, row_base+rows) are written); baseline: {table_id: DirtyBitmap}
+    of the since-baseline scope rebuilt for incremental sections (:476).
+    Errors are raised in the reference's order: the first failing section
+    wins; within a section FormatError precedes IntegrityError.
+    """
+    dev = device_of(device)
+    infos = parse_headers(data, incremental)  # FormatError for any bad header
+    if not infos:
+        return
+    L = _lib.lib()
+    buf = _upload_payload(data, dev)
+    flags = torch.zeros(len(infos), dtype=torch.int32, device=dev)
+    host_err = None
+    stream = _lib.stream_handle()
+    for k, info in enumerate(infos):
+        t = tables.get(info.table_id)
+        if t is None:
+            host_err = (k, IntegrityError(f"payload names unknown table {info.table_id}"))
+            break
+        if info.dim != t.dim:
+            host_err = (k, IntegrityError(f"dim mismatch in table {info.table_id}"))
+            break
+        if not incremental and info.rows != t.total_rows:
+            host_err = (k, IntegrityError(
+                f"full section for table {info.table_id} has {info.rows} rows, "
+                f"expected {t.total_rows}"))
+            break
+        bm = baseline.get(info.table_id) if (baseline is not None and incremental) else None
+        aux_ptr = t.aux.data_ptr() if (info.aux and t.aux is not None) else None
+        _lib.check(L.ds_restore_section(
+            buf.data_ptr() + info.body_offset, info.rows, info.dim, info.bitwidth or 0,
+            int(info.aux), int(incremental), t.total_rows, t.row_base, t.row_base + t.rows,
+            t.values.data_ptr(), t.values.stride(0), aux_ptr,
+            None if bm is None else bm.words.data_ptr(), flags[k:].data_ptr(), stream),
+            "restore_section")
+    fl = flags.cpu().numpy()
+    first_dev = next((k for k in range(len(infos)) if fl[k]), None)
+    if first_dev is not None and (host_err is None or first_dev < host_err[0]):
+        _lib.raise_flags(int(fl[first_dev]), f"restore (table {infos[first_dev].table_id})")
+    if host_err is not None:
+        raise host_err[1]
+
+
+@dataclass
+class RestoredTables:
+    """What restore produces on the GPU: device tables + rebuilt tracker."""
+
+    tables: dict
+    tracker: object
+    chain_ids: list = field(default_factory=list)
+    manifest: object = None
+    dense: np.ndarray | None = None
+
+
+def restore_chain(chain: list, table_shapes: dict, *, aux: bool = False, device=None,
+                  row_range: tuple | None = None) -> RestoredTables:
+    """Rebuild tables from a manifest chain (engine.py:443-512 scatter part).
+
+    chain: [(kind, [shard payload bytes, ...]), ...] in chain order (base
+    first; later entries override earlier ones); table_shapes: {tid: (rows,
+    dim)}; row_range=(lo, hi) restores only that global row range of every
+    table (one rank of a row-sharded restore).
+    """
+    from .tracker import ModelTracker
+
+    dev = device_of(device)
+    tables = {}
+    for tid, (rows, dim) in sorted(table_shapes.items()):
+        lo, hi = (0, rows) if row_range is None else (max(0, row_range[0]), min(rows, row_range[1]))
+        n = max(0, hi - lo)
+        tables[tid] = DeviceTable(tid, torch.zeros((n, dim), dtype=torch.float32, device=dev),
+                                  torch.zeros((n, dim), dtype=torch.float32, device=dev)
+                                  if aux else None, row_base=lo, total_rows=rows)
+    tracker = ModelTracker({tid: t.rows for tid, t in tables.items()}, device=dev)
+    baseline = {tid: tracker.baseline_bitmap(tid) for tid in tables}
+    for kind, payloads in chain:
+        inc = kind == INCREMENTAL
+        for data in payloads:
+            apply_payload(data, inc, tables, baseline if inc else None, device=dev)
+    return RestoredTables(tables=tables, tracker=tracker)
+
+
+def restore(cstore, *, fallback: bool = False, checkpoint_id: int | None = None,
+            device=None) -> RestoredTables:
+    """restore() over a reference-compatible CheckpointStore (engine.py:515-535).
+
+    Chain resolution and CRC verification are the store's (host, out of
+    scope); decoding and scattering run on the GPU.
+    """
+    def restore_at(cid):
+        chain = cstore.verify_chain(cid)
+        target = chain[-1]
+        shapes = {tid: (info.rows, info.dim) for tid, info in target.tables.items()}
+        plan = [(m.kind, [cstore.store.get(e.key) for _, e in sorted(m.shards.items())])
+                for m in chain]
+        out = restore_chain(plan, shapes, aux=bool(target.aux), device=device)
+        out.chain_ids = [m.checkpoint_id for m in chain]
+        out.manifest = target
+        out.dense = np.frombuffer(cstore.store.get(target.dense.key), dtype="<f4").astype(
+            np.float32)
+        return out
+
+    if checkpoint_id is not None:
+        return restore_at(checkpoint_id)
+    ids = cstore.valid_ids()
+    if not ids:
+        raise IntegrityError("no valid checkpoint to restore from")
+    last = None
+    for cid in reversed(ids):
+        try:
+            return restore_at(cid)
+        except Exception as exc:  # ours or the store's own IntegrityError/FormatError
+            if type(exc).__name__ not in ("IntegrityError", "FormatError") or not fallback:
+                raise
+            last = exc
+    raise IntegrityError(f"no restorable checkpoint: {last}")

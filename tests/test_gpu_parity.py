@@ -1,0 +1,365 @@
+"""GPU parity: the sm_100a path against the reference's golden fixtures and
+against the CPU oracle (bit-exact for ids, codes, params, bytes and restored
+float32 tables; err_sum within 1e-12 relative, see engine.py docstring)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+DIMS = (1, 3, 7, 8, 9, 16, 33, 64, 65, 128, 130)
+
+
+@pytest.fixture(scope="module")
+def ds():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2010_08679_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    return oracle
+
+
+def u32(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+def params_equal(a, b):
+    """float32 equality with +0 == -0 (the documented signed-zero exception)."""
+    return np.array_equal(np.asarray(a, np.float32), np.asarray(b, np.float32))
+
+
+# --- codec ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d", DIMS)
+@pytest.mark.parametrize("n", (2, 3, 4, 8))
+def test_codec_rows_match_golden(ds, golden, d, n):
+    g = golden("codec")
+    x = g[f"x_d{d}"]
+    lo, hi = ds.quant.row_minmax(x)
+    assert params_equal(lo, x.min(axis=1)) and params_equal(hi, x.max(axis=1))
+    codes = ds.quantize_rows(x, lo, hi, n)
+    assert np.array_equal(codes, g[f"codes_d{d}_n{n}"])
+    deq = ds.dequantize_rows(codes, lo, hi, n)
+    assert np.array_equal(u32(deq), u32(g[f"deq_d{d}_n{n}"]))
+    me = ds.reconstruction_errors(x, lo, hi, n)
+    assert np.array_equal(me.view(np.uint64), g[f"me_d{d}_n{n}"].view(np.uint64))
+    packed = ds.pack_code_rows(codes, n)
+    assert np.array_equal(packed, g[f"packed_d{d}_n{n}"])
+    assert np.array_equal(ds.unpack_code_rows(packed, n, d), codes)
+    if n != 8:
+        cfg = ds.default_adaptive_config(n)
+        amin, amax = ds.adaptive_params_rows(x, n, cfg)
+        assert np.array_equal(amin, g[f"amin_d{d}_n{n}"])
+        assert np.array_equal(amax, g[f"amax_d{d}_n{n}"])
+
+
+@pytest.mark.parametrize("n", (2, 3, 4))
+@pytest.mark.parametrize("bins,ratio", [(25, 0.5), (25, 0.2), (45, 0.2), (10, 0.3), (2, 1.0),
+                                        (1, 1.0)])
+def test_greedy_configs_match_golden(ds, golden, n, bins, ratio):
+    g = golden("codec")
+    amin, amax = ds.adaptive_params_rows(g["cfg_x"], n, ds.AdaptiveConfig(bins, ratio))
+    assert np.array_equal(amin, g[f"cfg_min_n{n}_b{bins}_r{ratio}"])
+    assert np.array_equal(amax, g[f"cfg_max_n{n}_b{bins}_r{ratio}"])
+
+
+def test_known_answers(ds):
+    assert ds.pack_codes([0, 1, 2, 3], 2) == b"\xe4"
+    p = ds.QuantParams(2, 0.0, 3.0)
+    assert ds.quantize(np.array([0.5, 1.5, 2.5], np.float32), p).codes.tolist() == [1, 2, 3]
+    x = np.array([-1.0, 0.0, 2.0], np.float32)
+    qv = ds.quantize(x, ds.uniform_params(x, 2))
+    assert qv.codes.tolist() == [0, 1, 3]
+    assert np.array_equal(ds.dequantize(qv), x)
+    c = np.full(9, 0.123, np.float32)
+    qv = ds.quantize(c, ds.uniform_params(c, 3))
+    assert not qv.codes.any() and np.array_equal(ds.dequantize(qv), c)
+    assert ds.quantize(np.array([-5.0, 5.0], np.float32),
+                       ds.QuantParams(4, -1.0, 1.0)).codes.tolist() == [0, 15]
+    with pytest.raises(ds.FormatError):
+        ds.unpack_codes(b"\xc0", 2, 3)
+    with pytest.raises(ds.FormatError):
+        ds.unpack_codes(b"\x00\x00", 2, 3)
+    with pytest.raises(ds.DataError):
+        ds.pack_codes([4], 2)
+    with pytest.raises(ds.FormatError):
+        ds.dequantize_rows(np.array([[0, 4]], np.uint8), np.zeros(1, np.float32),
+                           np.ones(1, np.float32), 2)
+    with pytest.raises(ds.DataError):
+        ds.adaptive_params_rows(np.array([[1.0, np.nan]], np.float32), 2,
+                                ds.default_adaptive_config(2))
+    with pytest.raises(ds.ConfigError):
+        ds.quantize_rows(np.zeros((1, 2), np.float32), np.zeros(1, np.float32),
+                         np.ones(1, np.float32), 5)
+
+
+def _edge_rows(d, rng):
+    rows = []
+    rows.append(np.full(d, 0.375, np.float32))                       # constant
+    rows.append((np.arange(d) % 5).astype(np.float32) * 0.25)        # grid: exact ties
+    rows.append((np.arange(d) % 3).astype(np.float32) - 1.0)         # symmetric grid
+    z = rng.normal(0, 1, d).astype(np.float32)
+    z[0] = -0.0
+    z[-1] = 0.0
+    rows.append(z)                                                    # signed zeros
+    o = rng.normal(0, 0.01, d).astype(np.float32)
+    o[d // 2] = 50.0
+    rows.append(o)                                                    # outlier
+    rows.append((rng.normal(0, 1, d) * 1e-30).astype(np.float32))     # tiny range
+    rows.append((rng.normal(0, 1, d) * 1e30).astype(np.float32))      # huge range
+    rows.append((rng.normal(1000, 1e-3, d)).astype(np.float32))       # offset >> range
+    rows.append(np.float32(rng.integers(-8, 8, d)) / 8)               # coarse grid
+    return np.stack(rows)
+
+
+@pytest.mark.parametrize("d", (1, 2, 5, 16, 31, 64, 128, 200, 1024))
+@pytest.mark.parametrize("n", (2, 3, 4, 8))
+def test_codec_edge_rows_vs_oracle(ds, O, d, n):
+    rng = np.random.default_rng(d * 10 + n)
+    x = np.concatenate([_edge_rows(d, rng),
+                        (rng.normal(0, 1, (300, d)) * rng.lognormal(0, 2, (300, 1))).astype(
+                            np.float32)])
+    lo, hi = O.row_minmax(x)
+    assert np.array_equal(ds.quantize_rows(x, lo, hi, n), O.quantize_rows(x, lo, hi, n))
+    assert np.array_equal(ds.reconstruction_errors(x, lo, hi, n),
+                          O.reconstruction_errors(x, lo, hi, n))
+    if n != 8:
+        bins, ratio = {2: (25, 0.5), 3: (25, 0.2), 4: (45, 0.2)}[n]
+        a = ds.adaptive_params_rows(x, n, ds.AdaptiveConfig(bins, ratio))
+        b = O.adaptive_params_rows(x, n, bins, ratio)
+        assert params_equal(a[0], b[0]) and params_equal(a[1], b[1])
+
+
+def test_adaptive_large_random_vs_oracle(ds, O):
+    """200k rows x 64 from the reference's benchmark distribution (quant.py:418-438)."""
+    rng = np.random.default_rng(42)
+    n, d = 200_000, 64
+    scale = np.exp(rng.normal(0, 1, n))
+    x = (rng.normal(0, 1, (n, d)) * scale[:, None] + (rng.normal(0.4, 0.3, n) * scale)[:, None])
+    cols = rng.integers(0, d, (n, 2))
+    x[np.arange(n)[:, None], cols] += rng.choice([-1, 1], (n, 2)) * rng.uniform(4, 8, (n, 2)) * \
+        scale[:, None]
+    x = x.astype(np.float32)
+    for nb in (2, 4):
+        bins, ratio = {2: (25, 0.5), 4: (45, 0.2)}[nb]
+        stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+        xd = torch.from_numpy(x).cuda()
+        a = ds.adaptive_params_rows(xd, nb, ds.AdaptiveConfig(bins, ratio), stats=stats)
+        b = O.adaptive_params_rows(x, nb, bins, ratio, nthreads=8)
+        assert np.array_equal(a[0].cpu().numpy(), b[0]) and np.array_equal(a[1].cpu().numpy(), b[1])
+        # the certified fast path decides almost everything in fp32
+        assert int(stats[0]) < 0.05 * n * 2 * (bins * ratio), int(stats[0])
+
+
+# --- tracker ---------------------------------------------------------------------
+
+def test_tracker_matches_golden(ds, golden):
+    g = golden("tracker")
+    rows = [int(r) for r in g["rows"]]
+    tr = ds.ModelTracker({t: r for t, r in enumerate(rows)})
+    for phase in range(3):
+        for t in range(len(rows)):
+            tr.mark(t, g[f"mark_p{phase}_t{t}"])
+        view = tr.capture()
+        for t in range(len(rows)):
+            assert np.array_equal(view.interval_rows[t], g[f"int_p{phase}_t{t}"])
+            assert np.array_equal(view.baseline_rows[t], g[f"base_p{phase}_t{t}"])
+        assert [view.interval_fraction, view.baseline_fraction] == g[f"frac_p{phase}"].tolist()
+        tr.reset_interval()
+
+
+def test_bitmap_semantics(ds):
+    bm = ds.DirtyBitmap(0, 1000)
+    assert bm.nbytes == 125
+    assert ds.DirtyBitmap(0, 9).nbytes == 2
+    bm.mark([3, 3, 3, 7, 999])
+    assert bm.popcount() == 3
+    assert bm.dirty_rows()[0].tolist() == [3, 7, 999]
+    with pytest.raises(ds.BoundsError):
+        bm.mark([1000])
+    with pytest.raises(IndexError):
+        bm.mark([-1])
+    assert bm.popcount() == 3
+    with pytest.raises(ds.ShapeError):
+        bm.merge_or(ds.DirtyBitmap(0, 999))
+    with pytest.raises(ds.ShapeError):
+        bm.merge_or(ds.DirtyBitmap(1, 1000))
+    other = ds.DirtyBitmap(0, 1000)
+    other.mark([5, 7])
+    u = bm.merge_or(other)
+    assert u.dirty_rows()[0].tolist() == [3, 5, 7, 999]
+    assert bm.dirty_rows()[0].tolist() == [3, 7, 999]
+    ref_bytes = np.zeros(125, np.uint8)
+    for r in (3, 5, 7, 999):
+        ref_bytes[r >> 3] |= 1 << (r & 7)
+    assert np.array_equal(u.to_bytes(), ref_bytes)
+    # device-tensor marks: deferred BoundsError at the next sync point
+    bm2 = ds.DirtyBitmap(0, 10)
+    bm2.mark(torch.tensor([1, 10], device="cuda"))
+    with pytest.raises(ds.BoundsError):
+        bm2.popcount()
+    tr = ds.ModelTracker({0: 8000, 1: 8000})
+    assert tr.nbytes() == 4 * 1000
+
+
+def test_capture_large_vs_oracle(ds, O):
+    rng = np.random.default_rng(1)
+    rows = {0: 3_000_000, 1: 65_537, 2: 1, 3: 1_000_003}
+    tr = ds.ModelTracker(rows)
+    ref_i = {t: np.zeros((r + 7) // 8, np.uint8) for t, r in rows.items()}
+    ref_b = {t: np.zeros((r + 7) // 8, np.uint8) for t, r in rows.items()}
+    for phase in range(2):
+        for t, r in rows.items():
+            idx = rng.integers(0, r, size=min(r * 2, 400_000))
+            tr.mark(t, idx)
+            O.mark(ref_i[t], r, idx)
+        view = tr.capture()
+        for t, r in rows.items():
+            assert np.array_equal(view.interval_rows[t], O.dirty_rows(ref_i[t], r))
+            assert np.array_equal(view.baseline_rows[t], O.dirty_rows(ref_i[t] | ref_b[t], r))
+            assert np.array_equal(tr.interval_bitmap(t).to_bytes(), ref_i[t])
+        tr.reset_interval()
+        for t in rows:
+            ref_b[t] |= ref_i[t]
+            ref_i[t][:] = 0
+
+
+def test_mark_batch_multi_table(ds, O):
+    rng = np.random.default_rng(3)
+    rows = {t: int(r) for t, r in enumerate(rng.integers(1, 200_000, 26))}
+    tr = ds.ModelTracker(rows)
+    idx, seg = [], [0]
+    for t, r in rows.items():
+        a = rng.integers(0, r, 5000)
+        idx.append(a)
+        seg.append(seg[-1] + a.size)
+    tr.mark_batch(torch.from_numpy(np.concatenate(idx)).cuda(), np.array(seg),
+                  np.array(list(rows)))
+    view = tr.capture()
+    for k, (t, r) in enumerate(rows.items()):
+        assert np.array_equal(view.interval_rows[t], np.unique(idx[k]))
+
+
+# --- writer ------------------------------------------------------------------------
+
+class _Snap:
+    def __init__(self, tables, nshards):
+        self.tables = tables
+        self.nshards = nshards
+
+    def shard_tables(self, sid):
+        return [self.tables[t] for t in sorted(self.tables) if t % self.nshards == sid]
+
+
+class _Tab:
+    def __init__(self, tid, values, aux=None):
+        self.table_id, self.values, self.aux = tid, values, aux
+
+
+class _Plan:
+    def __init__(self, kind, rows, bitwidth):
+        self.kind, self.rows, self.bitwidth = kind, rows, bitwidth
+
+
+@pytest.mark.parametrize("aux", (0, 1))
+@pytest.mark.parametrize("bw", (None, 2, 3, 4, 8))
+@pytest.mark.parametrize("kind", ("full", "incremental"))
+def test_payload_matches_golden(ds, golden, aux, bw, kind):
+    g = golden("payload")
+    tag = f"aux{aux}"
+    tabs = {t: _Tab(t, g[f"{tag}_values_t{t}"], g[f"{tag}_aux_t{t}"] if aux else None)
+            for t in range(3)}
+    rows = {t: g[f"{tag}_rows_t{t}"] for t in range(3)}
+    snap = _Snap(tabs, 2)
+    plan = _Plan(kind, rows if kind == "incremental" else None, bw)
+    for sid in range(2):
+        variants = [(None, "")] + ([({4: ds.AdaptiveConfig(1, 0.5)}, "_naive4")] if bw == 4 else [])
+        for ov, suffix in variants:
+            key = f"{tag}_bw{bw}_{kind}_s{sid}{suffix}"
+            blob, qr, err = ds.build_shard_payload(snap, plan, sid, 64, ov)
+            assert blob == g[key].tobytes(), key
+            want_q, want_err = g[key + "_meta"]
+            assert qr == want_q
+            assert err == pytest.approx(want_err, rel=1e-12, abs=0)
+
+
+@pytest.mark.parametrize("d", (1, 3, 8, 16, 20, 64, 100, 128, 256))
+@pytest.mark.parametrize("bw", (None, 2, 3, 4, 8))
+def test_payload_dims_vs_oracle(ds, O, d, bw):
+    rng = np.random.default_rng(d + (bw or 0))
+    rows = 3000
+    tabs = {t: _Tab(t, (rng.normal(0, 1, (rows, d)) * rng.lognormal(0, 1, (rows, 1))).astype(
+        np.float32), rng.random((rows, d)).astype(np.float32) if t == 1 else None)
+        for t in range(3)}
+    tabs[1].aux = None
+    sel = {t: np.sort(rng.choice(rows, rng.integers(0, rows), replace=False)) for t in range(3)}
+    sel[2] = np.zeros(0, np.int64)  # a 0-row table still gets its header
+    for kind in ("incremental", "full"):
+        plan = _Plan(kind, sel if kind == "incremental" else None, bw)
+        blob, qr, err = ds.build_shard_payload(_Snap(tabs, 1), plan, 0)
+        ref, qr_ref, err_ref = O.build_shard_payload(
+            {t: (tabs[t].values, None) for t in tabs}, kind, sel, bw, [0, 1, 2], nthreads=8)
+        assert blob == ref
+        assert qr == qr_ref
+        assert err == pytest.approx(err_ref, rel=1e-12, abs=1e-300)
+
+
+def test_writer_errors(ds):
+    x = np.zeros((10, 4), np.float32)
+    x[3, 1] = np.nan
+    snap = _Snap({0: _Tab(0, x)}, 1)
+    with pytest.raises(ds.DataError):
+        ds.build_shard_payload(snap, _Plan("full", None, 4), 0)
+    with pytest.raises(ds.BoundsError):
+        ds.build_shard_payload(_Snap({0: _Tab(0, np.zeros((10, 4), np.float32))}, 1),
+                               _Plan("incremental", {0: np.array([10])}, 8), 0)
+
+
+# --- restore ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("bw", (None, 3, 8))
+def test_restore_chain_matches_golden(ds, golden, bw):
+    g = golden("restore")
+    tag = f"bw{bw}"
+    rows, d = g[f"{tag}_values_t0"].shape
+    chain = []
+    for i in range(int(g[f"{tag}_nchain"])):
+        chain.append((str(g[f"{tag}_kind{i}"]), [g[f"{tag}_m{i}_s{s}"].tobytes() for s in range(2)]))
+    out = ds.restore_chain(chain, {0: (rows, d), 1: (rows, d)}, aux=True)
+    for t in range(2):
+        assert np.array_equal(u32(out.tables[t].values.cpu().numpy()), u32(g[f"{tag}_values_t{t}"]))
+        assert np.array_equal(u32(out.tables[t].aux.cpu().numpy()), u32(g[f"{tag}_aux_t{t}"]))
+        assert np.array_equal(out.tracker.since_baseline(t).dirty_rows()[0], g[f"{tag}_base_t{t}"])
+    # row-sharded restore: two halves reassemble the same tables
+    halves = [ds.restore_chain(chain, {0: (rows, d), 1: (rows, d)}, aux=True,
+                               row_range=(lo, hi)) for lo, hi in ((0, 77), (77, rows))]
+    for t in range(2):
+        cat = np.concatenate([h.tables[t].values.cpu().numpy() for h in halves])
+        assert np.array_equal(u32(cat), u32(g[f"{tag}_values_t{t}"]))
+
+
+def test_restore_errors(ds, O):
+    x = np.random.default_rng(0).normal(size=(4, 5)).astype(np.float32)
+    blob, _, _ = O.build_section(0, x, np.array([0, 2]), bitwidth=3)
+    shapes = {0: (4, 5)}
+    bad = bytearray(blob)
+    bad[24 + 16 + 1] |= 0x80
+    with pytest.raises(ds.FormatError):
+        ds.restore_chain([("incremental", [bytes(bad)])], shapes)
+    oob = bytearray(blob)
+    oob[24:32] = (4).to_bytes(8, "little")
+    with pytest.raises(ds.IntegrityError):
+        ds.restore_chain([("incremental", [bytes(oob)])], shapes)
+    with pytest.raises(ds.IntegrityError):
+        ds.restore_chain([("incremental", [blob])], {1: (4, 5)})
+    with pytest.raises(ds.IntegrityError):
+        ds.restore_chain([("incremental", [blob])], {0: (4, 6)})
+    with pytest.raises(ds.FormatError):
+        ds.restore_chain([("incremental", [blob + b"\x01"])], shapes)
