@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Checkpointed GB/s of embedding rows (track + compact + quantize + pack).
+
+Workload (BASELINE.json configs[1], "C2"): Criteo-Kaggle-shaped 26 tables
+(the published DLRM cardinalities, 33,762,577 rows) x dim 16 fp32, 8-bit
+quantization (naive ranges, the reference's 8-bit default), one checkpoint
+every 500 batches of 2048 Zipf(1.05) lookups per table.  One step = one
+checkpoint interval:
+  K1 mark the interval's 26 x 1,024,000 lookups into the dirty bitmaps,
+  K2 capture the interval's dirty ids + fold into the baseline scope,
+     (N > 1: NCCL all_gather of the per-table dirty counts),
+  K3 gather + quantize + pack the dirty rows into CNR1 records.
+Metric = sum of checkpointed fp32 row bytes (dirty rows x 64 B) / device time.
+Weak scaling: every rank owns a C2-sized row shard of 26 tables with N x the
+rows (rows [rank*card, (rank+1)*card) of each table).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's CPU path (the oracle port of
+deltasnap's tracker + build_shard_payload, oracle/) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CRITEO_KAGGLE = [1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683, 8351593,
+                 3194, 27, 14992, 5461306, 10, 5652, 2173, 4, 7046547, 18, 15, 286181, 105, 142572]
+DIM = 16
+BITWIDTH = 8
+BATCHES = 500
+BATCH = 2048
+ZIPF_S = 1.05
+METRIC = "checkpointed GB/s of embedding rows (track+quantize+pack) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--tables", type=int, default=len(CRITEO_KAGGLE),
+                   help="use the first T tables (smoke/profiling only)")
+    p.add_argument("--l2-fetch", type=int, default=64,
+                   help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default)")
+    return p.parse_args()
+
+
+def workload_desc(cards, n_lookups_per_table):
+    return {
+        "workload": "C2: Criteo-Kaggle-shaped 26 tables x dim 16 fp32, 8-bit naive, "
+                    "checkpoint every 500 batches x 2048 Zipf(1.05) lookups/table",
+        "tables": len(cards), "rows_per_rank": int(sum(cards)), "dim": DIM,
+        "bitwidth": BITWIDTH, "batches_per_interval": BATCHES, "batch": BATCH,
+        "lookups_per_step_per_rank": int(n_lookups_per_table * len(cards)),
+        "lookup_dtype": "int32", "scope": "interval (consecutive increments)",
+        "row_map": "Zipf rank -> row through a seeded permutation per table",
+        "l2": "inputs larger than L2 (2.16 GB tables, 107 MB lookups per step and rank)",
+    }
+
+
+# --------------------------------------------------------------------------------
+# clocks (NVML polled every ~2 ms during the timed region)
+# --------------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # NVML unavailable: report what we have
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------
+# synthetic workload
+# --------------------------------------------------------------------------------
+
+def zipf_lookups_torch(rows, n, gen, device):
+    import torch
+    w = torch.arange(1, rows + 1, dtype=torch.float64, device=device).pow_(-ZIPF_S)
+    cdf = torch.cumsum(w, 0)
+    cdf /= cdf[-1].clone()
+    u = torch.rand(n, dtype=torch.float64, generator=gen, device=device)
+    ranks = torch.searchsorted(cdf, u, right=True).clamp_(max=rows - 1)
+    perm = torch.randperm(rows, generator=gen, device=device)
+    return perm[ranks].to(torch.int32)
+
+
+def zipf_lookups_numpy(rows, n, rng):
+    w = np.arange(1, rows + 1, dtype=np.float64) ** -ZIPF_S
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    ranks = np.minimum(np.searchsorted(cdf, rng.random(n), side="right"), rows - 1)
+    return rng.permutation(rows)[ranks].astype(np.int32)
+
+
+# --------------------------------------------------------------------------------
+# CPU path (the oracle port of the reference: tracker.py + build_shard_payload)
+# --------------------------------------------------------------------------------
+
+class CpuPath:
+    """Reference CPU path on host arrays, all host threads.
+
+    Per step: DirtyBitmap.mark of every table's lookups (tracker.py:27-36),
+    capture of the interval scope (tracker.py:54-58) + reset_interval
+    (:120-124), then build_shard_payload's incremental 8-bit section per
+    table (engine.py:139-187).  Tables run in parallel threads (ctypes
+    releases the GIL); rows of a section run on OpenMP threads.
+    """
+
+    def __init__(self, tables, lookups, cards, threads):
+        from oracle import oracle as O
+        self.O = O
+        self.tables, self.lookups, self.cards = tables, lookups, cards
+        self.threads = threads
+        self.bits = [np.zeros((r + 7) // 8, np.uint8) for r in cards]
+        self.base = [np.zeros((r + 7) // 8, np.uint8) for r in cards]
+        from concurrent.futures import ThreadPoolExecutor
+        self.pool = ThreadPoolExecutor(max_workers=threads)
+
+    def step(self, tables_subset=None):
+        O = self.O
+        ts = range(len(self.cards)) if tables_subset is None else tables_subset
+
+        def track(t):
+            O.mark(self.bits[t], self.cards[t], self.lookups[t])
+            ids = O.dirty_rows(self.bits[t], self.cards[t])
+            self.base[t] |= self.bits[t]
+            self.bits[t][:] = 0
+            return ids
+
+        ids = list(self.pool.map(track, ts))
+        big = [k for k, t in enumerate(ts) if ids[k].size > 65536]
+        small = [k for k, t in enumerate(ts) if ids[k].size <= 65536]
+
+        def build(k, nthreads):
+            t = list(ts)[k]
+            return O.build_section(t, self.tables[t], ids[k], bitwidth=BITWIDTH, adaptive=None,
+                                   nthreads=nthreads)
+
+        outs = list(self.pool.map(lambda k: build(k, 1), small))
+        for k in big:
+            outs.append(build(k, self.threads))
+        rows = sum(i.size for i in ids)
+        return rows, sum(len(o[0]) for o in outs)
+
+
+# --------------------------------------------------------------------------------
+
+def run_reference(args):
+    """--impl reference: the CPU path on the host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cards = CRITEO_KAGGLE[:args.tables]
+    rng = np.random.default_rng(args.seed)
+    tables = [(rng.random((r, DIM), dtype=np.float32) * 2 - 1) for r in cards]
+    n_look = BATCHES * BATCH
+    lookups = [zipf_lookups_numpy(r, n_look, rng) for r in cards]
+    threads = os.cpu_count() or 1
+    cpu = CpuPath(tables, lookups, cards, threads)
+    for _ in range(max(1, args.warmup)):
+        cpu.step()
+    t0 = time.perf_counter()
+    rows_total = 0
+    for _ in range(args.steps):
+        rows, _ = cpu.step()
+        rows_total += rows
+    dt = time.perf_counter() - t0
+    value = rows_total * DIM * 4 / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": workload_desc(cards, n_look),
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": "full C2 interval per step (all 26 tables, 26.6M lookups)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2010_08679_b200 as ds
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2010_08679_b200 import _lib as dslib
+    if args.l2_fetch:
+        dslib.check(dslib.lib().ds_set_l2_fetch_granularity(args.l2_fetch), "l2 fetch")
+    l2_fetch = int(dslib.lib().ds_get_l2_fetch_granularity())
+
+    cards = CRITEO_KAGGLE[:args.tables]
+    n_look = BATCHES * BATCH
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed * 7919 + rank)
+    tables = []
+    for t, r in enumerate(cards):
+        v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
+        tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
+    lookups = [zipf_lookups_torch(r, n_look, gen, dev) for r in cards]
+    idx = torch.cat(lookups)
+    seg_off = np.arange(len(cards) + 1, dtype=np.int64) * n_look
+    seg_tab = np.arange(len(cards))
+    ck = ShardedCheckpointer(tables, BITWIDTH, rank=rank, world_size=world, device=dev)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up: W steps, then keep stepping until the clocks have ramped (>= 0.3 s)
+    for _ in range(max(3, args.warmup)):
+        ck.step(idx, seg_off, seg_tab)
+    torch.cuda.synchronize()
+    t_end = time.perf_counter() + 0.3
+    while time.perf_counter() < t_end:
+        ck.step(idx, seg_off, seg_tab)
+        torch.cuda.synchronize()
+    ck.fetch()  # raises any flagged data error of the warm-up steps
+
+    # ---- device-timed region: exactly K steps --------------------------------------
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        start.record()
+        for k in range(K):
+            ev[k][0].record()
+            ck.mark(idx, seg_off, seg_tab)                 # K1
+            ev[k][1].record()
+            ck.tracker.capture_into(ck.ids, ck.counts, fold=1, scope=ck.scope)   # K2
+            if world > 1:
+                dist.all_gather_into_tensor(ck.all_counts, ck.counts)
+            ev[k][2].record()
+            ck.writer.write(ck.payload, ck.ids, ck.counts[:ck.nt], None, local_ids=True)  # K3
+            ev[k][3].record()
+        stop.record()
+        torch.cuda.synchronize()
+    barrier()
+    elapsed = max_over_ranks(start.elapsed_time(stop) / 1e3)
+    phase = np.array([[ev[k][j].elapsed_time(ev[k][j + 1]) for j in range(3)] for k in range(K)])
+    t_mark, t_cap, t_write = phase.mean(axis=0) / 1e3
+
+    nbytes, local, per_table, _, _ = ck.layout()
+    dirty_rank = int(local.sum())
+    dirty_all = int(per_table.sum())  # every rank's dirty rows (from the count all_gather)
+    row_bytes = DIM * 4
+    value = dirty_all * row_bytes * K / elapsed / 1e9
+    _ = ck.fetch()  # error flags of the timed steps
+
+    # roofline of the dominant kernel (algorithmic bytes / its mean duration)
+    rec = ck.rec
+    k1_bytes = n_look * len(cards) * 4
+    k3_bytes = dirty_rank * (row_bytes + 8 + rec) + len(cards) * 24
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if peaks else "fallback"
+    phases = {
+        "mark": {"ms": t_mark * 1e3, "bytes": k1_bytes, "GB/s": k1_bytes / t_mark / 1e9},
+        "capture": {"ms": t_cap * 1e3},
+        "write": {"ms": t_write * 1e3, "bytes": k3_bytes, "GB/s": k3_bytes / t_write / 1e9},
+    }
+    dom = "mark" if t_mark >= t_write else "write"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    roofline = {"bound": "hbm", "kernel": {"mark": "ds::mark_kernel",
+                                           "write": "ds::writer_kernel<4,1,4,1,false>"}[dom],
+                "achieved": phases[dom]["GB/s"], "peak": peak, "unit": "GB/s",
+                "frac": phases[dom]["GB/s"] / peak, "traffic": traffic,
+                "peak_source": peak_src}
+
+    # ---- e2e through the public API with host buffers --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        idx_host = idx.cpu().pin_memory()
+        idx_dev = torch.empty_like(idx)
+        out = torch.empty(ck.capacity + 16, dtype=torch.uint8, pin_memory=True)
+        h2d = idx_host.numel() * idx_host.element_size()
+        d2h = 0
+
+        def e2e_step():
+            idx_dev.copy_(idx_host, non_blocking=True)                    # H2D inputs
+            ck.step(idx_dev, seg_off, seg_tab)
+            _, n = ck.fetch(out)                                          # D2H result
+            torch.cuda.current_stream().synchronize()
+            return n
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e_start.record()
+        for _ in range(K):
+            d2h = e2e_step()
+        e_stop.record()
+        torch.cuda.synchronize()
+        barrier()
+        e_el = max_over_ranks(e_start.elapsed_time(e_stop) / 1e3)
+        e2e = {"value": dirty_all * row_bytes * K / e_el / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e_el / K * 1e3}
+
+    # ---- CPU baseline (rank 0, N == 1): oracle port on the same inputs ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        host_tables = [t.values.cpu().numpy() for t in tables]
+        host_look = [lk.cpu().numpy() for lk in lookups]
+        threads = os.cpu_count() or 1
+        cp = CpuPath(host_tables, host_look, cards, threads)
+        cp.step()
+        t0 = time.perf_counter()
+        rows_c, reps = 0, 0
+        while reps < 3 and (reps == 0 or time.perf_counter() - t0 < 20):
+            r, _ = cp.step()
+            rows_c += r
+            reps += 1
+        dt = time.perf_counter() - t0
+        cpu = {"value": rows_c * row_bytes / dt / 1e9, "unit": "GB/s", "cores": threads,
+               "kind": "port",
+               "sample": f"{reps} full C2 interval(s): mark 26.6M lookups, capture, "
+                         "8-bit sections of every dirty row"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": elapsed / K * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": dict(workload_desc(cards, n_look), dirty_rows_per_step=dirty_all,
+                           parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch),
+            "rows_per_s": dirty_all * K / elapsed,
+            "roofline": roofline, "phases": phases,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "gpu_launches": K * 7,
+            "payload_bytes_per_step": int(nbytes) if world == 1 else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -67,6 +67,10 @@ typedef enum {
 DS_API const char *ds_version(void);
 DS_API const char *ds_last_error(void); /* thread-local text of the last non-OK status */
 DS_API int ds_device_sm_count(int device);
+/* Process-wide HBM fetch size of an L2 miss on the current device (0..128 B;
+ * cudaLimitMaxL2FetchGranularity).  64 suits the dim-16 row gather. */
+DS_API int ds_set_l2_fetch_granularity(int bytes);
+DS_API int ds_get_l2_fetch_granularity(void);
 
 /* ------------------------------------------------------------------ */
 /* K1 / tracking (tracker.py:27-36, :91-92, :132-134)                   */
@@ -80,6 +84,12 @@ DS_API int ds_device_sm_count(int device);
 DS_API int ds_mark(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
             const int64_t *idx, const int64_t *seg_off_host, const int32_t *seg_table_host,
             int nseg, uint32_t *flags, void *stream);
+
+/* Same with int32 ids (lookup streams of tables below 2^31 rows): halves the
+ * index bytes K1 streams. */
+DS_API int ds_mark_i32(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+                       const int32_t *idx, const int64_t *seg_off_host,
+                       const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream);
 
 /* Single-table convenience form (DirtyBitmap.mark). */
 DS_API int ds_mark_table(uint32_t *words, int64_t rows, const int64_t *idx, int64_t n, uint32_t *flags,
@@ -141,6 +151,10 @@ typedef struct {
     int adaptive_steps; /* floor(num_bins*ratio + 1e-9) (quant.py:186) */
     int write_headers;  /* 1: write the 24-byte CNR1 section headers */
     int aux;            /* 1: aux_flag set, aux rows appended (payload.py:102-103) */
+    int ids_packed;     /* 1: table t's ids start at sum(counts[<t]) (capture's layout);
+                           ds_table_desc.ids_off is then ignored */
+    int ids_local;      /* 1: ids are table-local rows (capture output); the record
+                           carries row_base + id */
     unsigned long long *stats; /* optional device counters (DS_STAT_*), may be NULL */
 } ds_ckpt_params;
 

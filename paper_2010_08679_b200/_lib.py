@@ -62,6 +62,8 @@ class CkptParams(ctypes.Structure):
         ("adaptive_steps", ctypes.c_int),
         ("write_headers", ctypes.c_int),
         ("aux", ctypes.c_int),
+        ("ids_packed", ctypes.c_int),
+        ("ids_local", ctypes.c_int),
         ("stats", ctypes.c_void_p),
     ]
 
@@ -75,7 +77,10 @@ _SIGNATURES = {
     "ds_version": (ctypes.c_char_p, []),
     "ds_last_error": (ctypes.c_char_p, []),
     "ds_device_sm_count": (_I, [_I]),
+    "ds_set_l2_fetch_granularity": (_I, [_I]),
+    "ds_get_l2_fetch_granularity": (_I, []),
     "ds_mark": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P]),
+    "ds_mark_i32": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P]),
     "ds_mark_table": (_I, [_P, _I64, _P, _I64, _P, _P]),
     "ds_bitmap_op": (_I, [_P, _P, _P, _I64, _I, _P]),
     "ds_popcount": (_I, [_P, _I64, _P, _P]),

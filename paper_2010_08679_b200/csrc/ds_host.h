@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/deltasnap_cuda.h"
 
@@ -32,6 +33,12 @@ inline int check_launch(const char *what) {
 
 // SM count of the current device, cached per device (read-only after init).
 int sm_count();
+
+// Diagnostic switches (A/B measurements), read from the environment.
+inline bool env_flag(const char *name) {
+    const char *v = getenv(name);
+    return v && v[0] && v[0] != '0';
+}
 
 // Grid for a grid-stride kernel: enough blocks to cover n, capped at
 // `per_sm` resident blocks per SM.

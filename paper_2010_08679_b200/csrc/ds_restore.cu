@@ -28,6 +28,7 @@ struct RestoreArgs {
     int dim, bitwidth, L, aux, incremental;
     int rec, par_off, code_off, packed, aux_off;
     int tile_rows;
+    double invL;
 };
 
 __device__ __forceinline__ uint32_t ld4_unaligned_g(const uint8_t *p) {
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(RT) restore_kernel(const RestoreArgs a) {
                     uhi |= (uint32_t)rec[a.par_off + 4 + k] << (8 * k);
                 }
                 const float lo = __uint_as_float(ulo), hi = __uint_as_float(uhi);
-                const double s = scale64(lo, hi, a.L);
+                const double s = scale64_y(lo, hi, (double)a.L, a.invL);
                 const uint8_t *pk = rec + a.code_off;
                 const int N = a.bitwidth;
                 for (int e = lig; e < d; e += G) {
@@ -153,6 +154,7 @@ extern "C" int ds_restore_section(const uint8_t *body, int64_t nrec, int64_t dim
     a.dim = (int)dim;
     a.bitwidth = bitwidth;
     a.L = bitwidth ? (1 << bitwidth) - 1 : 0;
+    a.invL = bitwidth ? 1.0 / (double)a.L : 0.0;
     a.aux = aux;
     a.incremental = incremental;
     a.rec = (int)ds_record_size(dim, bitwidth, aux, incremental);

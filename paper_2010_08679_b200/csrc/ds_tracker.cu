@@ -18,19 +18,60 @@ namespace ds {
 // ---------------------------------------------------------------------------
 struct MarkArgs {
     uint32_t *words;
-    const int64_t *idx;
+    const void *idx;
+    int idx32;  // 1: int32 ids, 0: int64 ids
     uint32_t *flags;
     int64_t word_off[DS_MAX_TABLES];
     int64_t rows[DS_MAX_TABLES];
     int64_t seg_off[DS_MAX_TABLES + 1];
     int32_t seg_table[DS_MAX_TABLES];
+    int blk_off[DS_MAX_TABLES + 1];  // TMA kernel: first CTA of each segment
     int nseg;
 };
 
-__global__ void __launch_bounds__(256) mark_kernel(const MarkArgs a) {
+// Each CTA marks one contiguous range of the lookup stream (so it sees a
+// table's Zipf head over and over), 8 ids per thread per iteration from
+// 128-bit loads.  A direct-mapped shared-memory cache remembers bitmap words
+// whose bits this CTA already knows to be set: a repeat of a hot row costs a
+// shared-memory probe instead of an L2 round trip to one contended word.
+// Cache entries are (word+1) << 32 | known_bits written with one 64-bit store,
+// so a racing update can only lose knowledge, never invent a set bit.
+constexpr int MARK_THREADS = 256;
+constexpr int MARK_PER_THREAD = 8;
+constexpr int MARK_CACHE = 1024;  // entries (8 KB)
+
+template <typename IdxT>
+__device__ __forceinline__ void load8(const IdxT *p, int64_t i, int64_t end, bool vec,
+                                      int64_t (&r)[MARK_PER_THREAD]) {
+    if (vec && i + MARK_PER_THREAD <= end) {
+        if (sizeof(IdxT) == 4) {
+            const int4 *q = reinterpret_cast<const int4 *>(p + i);
+            int4 u = __ldcs(q), v = __ldcs(q + 1);  // streamed once
+            r[0] = u.x; r[1] = u.y; r[2] = u.z; r[3] = u.w;
+            r[4] = v.x; r[5] = v.y; r[6] = v.z; r[7] = v.w;
+        } else {
+            const longlong2 *q = reinterpret_cast<const longlong2 *>(p + i);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                longlong2 u = __ldcs(q + k);
+                r[2 * k] = u.x;
+                r[2 * k + 1] = u.y;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < MARK_PER_THREAD; k++)
+            r[k] = i + k < end ? (int64_t)__ldcs(p + i + k) : -1;
+    }
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(MARK_THREADS) mark_kernel(const MarkArgs a, int64_t per_block,
+                                                           int vec, int use_cache) {
     __shared__ int64_t s_seg_off[DS_MAX_TABLES + 1];
     __shared__ int64_t s_base[DS_MAX_TABLES];
     __shared__ int64_t s_rows[DS_MAX_TABLES];
+    __shared__ unsigned long long cache[MARK_CACHE];
     for (int s = threadIdx.x; s <= a.nseg; s += blockDim.x) {
         s_seg_off[s] = a.seg_off[s];
         if (s < a.nseg) {
@@ -38,25 +79,261 @@ __global__ void __launch_bounds__(256) mark_kernel(const MarkArgs a) {
             s_rows[s] = a.rows[a.seg_table[s]];
         }
     }
+    for (int k = threadIdx.x; k < MARK_CACHE; k += blockDim.x) cache[k] = 0ull;
     __syncthreads();
+    const IdxT *idx = static_cast<const IdxT *>(a.idx);
     const int64_t total = s_seg_off[a.nseg];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t start = s_seg_off[0] + (int64_t)blockIdx.x * per_block;
+    const int64_t end = min(total, start + per_block);
     bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        int64_t r = __ldcs(a.idx + i);  // streamed once: do not keep in L2
-        int lo = 0, hi = a.nseg - 1;     // segment of i: largest s with seg_off[s] <= i
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (s_seg_off[mid] <= i) lo = mid;
-            else hi = mid - 1;
+    int seg = 0;
+    for (int64_t i = start + (int64_t)threadIdx.x * MARK_PER_THREAD; i < end;
+         i += (int64_t)MARK_THREADS * MARK_PER_THREAD) {
+        int64_t r[MARK_PER_THREAD];
+        load8<IdxT>(idx, i, end, vec, r);
+        while (i >= s_seg_off[seg + 1]) seg++;  // ranges only move forward
+        // word ids fit 32 bits (checked on the host); the 8 ids usually share
+        // one segment, else fall back to a per-id segment walk
+        const bool one_seg = i + MARK_PER_THREAD <= s_seg_off[seg + 1] && i + MARK_PER_THREAD <= end;
+        uint32_t w[MARK_PER_THREAD], bit[MARK_PER_THREAD], old[MARK_PER_THREAD];
+        uint32_t slot[MARK_PER_THREAD];
+        bool need[MARK_PER_THREAD];
+        if (one_seg) {
+            const uint32_t base = (uint32_t)s_base[seg];
+            const uint64_t rows = (uint64_t)s_rows[seg];
+#pragma unroll
+            for (int k = 0; k < MARK_PER_THREAD; k++) {
+                need[k] = (uint64_t)r[k] < rows;  // negative ids wrap to huge
+                bad |= !need[k];
+                uint32_t u = (uint32_t)r[k];
+                w[k] = base + (u >> 5);
+                bit[k] = 1u << (u & 31);
+                slot[k] = (w[k] * 2654435761u) >> (32 - 10);
+            }
+        } else {
+            int sg = seg;
+#pragma unroll
+            for (int k = 0; k < MARK_PER_THREAD; k++) {
+                need[k] = false;
+                w[k] = bit[k] = slot[k] = 0;
+                if (i + k >= end) continue;
+                while (i + k >= s_seg_off[sg + 1]) sg++;
+                if ((uint64_t)r[k] >= (uint64_t)s_rows[sg]) {
+                    bad = true;
+                    continue;
+                }
+                uint32_t u = (uint32_t)r[k];
+                w[k] = (uint32_t)s_base[sg] + (u >> 5);
+                bit[k] = 1u << (u & 31);
+                slot[k] = (w[k] * 2654435761u) >> (32 - 10);
+                need[k] = true;
+            }
         }
-        if (r < 0 || r >= s_rows[lo]) {
-            bad = true;
-            continue;
+        if (use_cache) {
+#pragma unroll
+            for (int k = 0; k < MARK_PER_THREAD; k++) {
+                unsigned long long e = cache[slot[k]];
+                // this CTA already knows the bit is set
+                if ((uint32_t)(e >> 32) == w[k] + 1 && ((uint32_t)e & bit[k])) need[k] = false;
+            }
         }
-        uint32_t *w = a.words + s_base[lo] + (r >> 5);
-        uint32_t bit = 1u << (r & 31);
-        if (!(__ldcg(w) & bit)) atomicOr(w, bit);
+        // all L2 probes in flight together, then the atomics
+#pragma unroll
+        for (int k = 0; k < MARK_PER_THREAD; k++) old[k] = need[k] ? __ldcg(a.words + w[k]) : 0u;
+#pragma unroll
+        for (int k = 0; k < MARK_PER_THREAD; k++) {
+            if (!need[k]) continue;
+            if (!(old[k] & bit[k])) atomicOr(a.words + w[k], bit[k]);
+            if (use_cache)
+                cache[slot[k]] = ((unsigned long long)(w[k] + 1) << 32) | (old[k] | bit[k]);
+        }
+    }
+    if (__any_sync(DS_FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
+}
+
+// ---------------------------------------------------------------------------
+// K1, TMA form: the lookup stream is pulled into shared memory by the Tensor
+// Memory Accelerator (cp.async.bulk, 16 KB per stage, 4 stages, mbarrier
+// completion), so the HBM stream needs no registers and no issue slots.
+// Threads probe a direct-mapped shared cache of (word, bits known set); a miss
+// issues a fire-and-forget RED.OR (no dependent L2 round trip) and records the
+// bit.  Correct for any interleaving: bits are only ever set, and a cache
+// entry only claims bits this CTA has itself OR-ed (or seen OR-ed) into HBM.
+// ---------------------------------------------------------------------------
+constexpr int MK_STAGES = 4;
+constexpr int MK_STAGE_BYTES = 8192;  // 2048 int32 ids: 8 per thread
+constexpr int MK_CACHE_BITS = 11;      // 2048 entries (16 KB)
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes,
+                                            unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Every CTA works inside ONE segment (one table's slice of the lookup
+// stream); the host gives each segment ceil(len / per_block) CTAs.
+//  * small tables (bitmap <= MK_WIN_WORDS words): the CTA ORs into a
+//    shared-memory copy of the table's bitmap (ATOMS, no HBM traffic) and at
+//    the end ORs each non-zero word into HBM once (RED);
+//  * large tables: shared cache of (word, bits known set) with second-chance
+//    replacement; a miss issues one RED.OR (fire and forget).
+// Correct for any interleaving: bits are only ever set, and a cache entry
+// only claims bits this CTA itself OR-ed into HBM.
+constexpr int MK_WIN_WORDS = 2048;  // 65536 rows: 18 of the 26 Criteo-Kaggle tables
+
+template <typename IdxT>
+__global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a, int64_t per_block,
+                                                               int unused) {
+    constexpr int IDS = MK_STAGE_BYTES / (int)sizeof(IdxT);  // ids per stage
+    constexpr int PER_THREAD = IDS / MARK_THREADS;            // 8 (int32) or 4 (int64)
+    extern __shared__ __align__(128) uint8_t mk_smem[];
+    IdxT *buf = reinterpret_cast<IdxT *>(mk_smem);
+    __shared__ __align__(8) unsigned long long bars[MK_STAGES];
+    __shared__ unsigned long long cache[1 << MK_CACHE_BITS];  // large tables
+    uint32_t *win = reinterpret_cast<uint32_t *>(cache);      // small tables (aliases the cache)
+    static_assert(MK_WIN_WORDS * 4 <= (1 << MK_CACHE_BITS) * 8, "window must fit the cache");
+    // segment of this CTA: last s with blk_off[s] <= blockIdx.x
+    int seg = 0;
+    while (seg + 1 < a.nseg && a.blk_off[seg + 1] <= (int)blockIdx.x) seg++;
+    const int64_t s0 = a.seg_off[seg], s1 = a.seg_off[seg + 1];
+    const int64_t start = s0 + (int64_t)(blockIdx.x - a.blk_off[seg]) * per_block;
+    const int64_t end = min(s1, start + per_block);
+    const uint32_t base = (uint32_t)a.word_off[a.seg_table[seg]];
+    const uint64_t rows = (uint64_t)a.rows[a.seg_table[seg]];
+    const uint32_t nwords = (uint32_t)((rows + 31) / 32);
+    const bool small = nwords <= (uint32_t)MK_WIN_WORDS;
+    for (int k = threadIdx.x; k < (1 << MK_CACHE_BITS); k += MARK_THREADS) cache[k] = 0ull;
+    const IdxT *idx = static_cast<const IdxT *>(a.idx);
+    // TMA moves whole 16-byte units; the ragged tail (< 16 B) is read directly
+    const int64_t bulk_end =
+        start + ((end - start) * (int64_t)sizeof(IdxT) / 16) * 16 / (int64_t)sizeof(IdxT);
+    const int nch = (int)((bulk_end - start + IDS - 1) / IDS);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < MK_STAGES; s++) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < MK_STAGES && k < nch; k++) {
+            int64_t c0 = start + (int64_t)k * IDS;
+            unsigned bytes = (unsigned)(min((int64_t)IDS, bulk_end - c0) * sizeof(IdxT));
+            mbar_expect_tx(&bars[k], bytes);
+            tma_load_1d(buf + (size_t)k * IDS, idx + c0, bytes, &bars[k]);
+        }
+    }
+    bool bad = false;
+    // Cache entry: key (word+1, 31 bits) << 33 | referenced << 32 | bits known
+    // set.  Second-chance replacement keeps the Zipf head cached.
+    auto cache_mark = [&](uint32_t w, uint32_t bit, uint32_t slot, unsigned long long e) {
+        const bool match = (uint32_t)(e >> 33) == w + 1;
+        const uint32_t known = match ? (uint32_t)e : 0u;
+        if (known & bit) {
+            if (!(e & (1ull << 32))) cache[slot] = e | (1ull << 32);  // referenced
+            return;
+        }
+        atomicOr(a.words + w, bit);  // result unused -> RED, no round trip
+        if (match) cache[slot] = e | bit | (1ull << 32);
+        else if (e & (1ull << 32)) cache[slot] = e & ~(1ull << 32);  // second chance
+        else cache[slot] = ((unsigned long long)(w + 1) << 33) | bit;
+    };
+    auto mark_row = [&](uint32_t u) {
+        if (small) {
+            atomicOr(win + (u >> 5), 1u << (u & 31));  // shared-memory OR
+        } else {
+            const uint32_t w = base + (u >> 5);
+            const uint32_t slot = (w * 2654435761u) >> (32 - MK_CACHE_BITS);
+            cache_mark(w, 1u << (u & 31), slot, cache[slot]);
+        }
+    };
+    for (int k = 0; k < nch; k++) {
+        const int s = k % MK_STAGES;
+        mbar_wait(&bars[s], (unsigned)(k / MK_STAGES) & 1u);
+        const int64_t c0 = start + (int64_t)k * IDS;
+        const int cnt = (int)min((int64_t)IDS, bulk_end - c0);
+        const IdxT *b = buf + (size_t)s * IDS;
+        const int j0 = threadIdx.x * PER_THREAD;
+        if (j0 + PER_THREAD <= cnt) {
+            IdxT v[PER_THREAD];
+#pragma unroll
+            for (int q = 0; q < PER_THREAD * (int)sizeof(IdxT) / 16; q++)
+                reinterpret_cast<int4 *>(v)[q] = reinterpret_cast<const int4 *>(b + j0)[q];
+            if (small) {
+#pragma unroll
+                for (int q = 0; q < PER_THREAD; q++) {
+                    const bool ok = (uint64_t)(int64_t)v[q] < rows;  // negatives wrap high
+                    bad |= !ok;
+                    if (ok) atomicOr(win + ((uint32_t)v[q] >> 5), 1u << ((uint32_t)v[q] & 31));
+                }
+            } else {
+                // all cache probes before any update so their latencies overlap
+                uint32_t w[PER_THREAD], slot[PER_THREAD];
+                unsigned long long e[PER_THREAD];
+                bool ok[PER_THREAD];
+#pragma unroll
+                for (int q = 0; q < PER_THREAD; q++) {
+                    ok[q] = (uint64_t)(int64_t)v[q] < rows;
+                    bad |= !ok[q];
+                    w[q] = base + ((uint32_t)v[q] >> 5);
+                    slot[q] = (w[q] * 2654435761u) >> (32 - MK_CACHE_BITS);
+                    e[q] = cache[slot[q]];
+                }
+#pragma unroll
+                for (int q = 0; q < PER_THREAD; q++)
+                    if (ok[q]) cache_mark(w[q], 1u << ((uint32_t)v[q] & 31), slot[q], e[q]);
+            }
+        } else {
+            for (int q = j0; q < cnt && q < j0 + PER_THREAD; q++) {
+                const int64_t r = (int64_t)b[q];
+                if ((uint64_t)r >= rows) bad = true;
+                else mark_row((uint32_t)r);
+            }
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0 && k + MK_STAGES < nch) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            int64_t c1 = start + (int64_t)(k + MK_STAGES) * IDS;
+            unsigned bytes = (unsigned)(min((int64_t)IDS, bulk_end - c1) * sizeof(IdxT));
+            mbar_expect_tx(&bars[s], bytes);
+            tma_load_1d(buf + (size_t)s * IDS, idx + c1, bytes, &bars[s]);
+        }
+    }
+    // ragged tail
+    for (int64_t i = bulk_end + threadIdx.x; i < end; i += MARK_THREADS) {
+        const int64_t r = (int64_t)idx[i];
+        if ((uint64_t)r >= rows) bad = true;
+        else mark_row((uint32_t)r);
+    }
+    if (small) {  // flush the window: one RED per touched word
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < nwords; k += MARK_THREADS) {
+            const uint32_t v = win[k];
+            if (v) atomicOr(a.words + base + k, v);
+        }
     }
     if (__any_sync(DS_FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
 }
@@ -289,18 +566,203 @@ __global__ void __launch_bounds__(CAP_THREADS) capture_write_kernel(const CapArg
     }
 }
 
+// ---------------------------------------------------------------------------
+// K2, single pass: chunks of 1024 words (4 consecutive words per thread) are
+// claimed in dispatch order through a ticket; each chunk popcounts both scopes,
+// scans them inside the CTA, and resolves its global offset by a decoupled
+// look-back over its predecessors' published (aggregate | inclusive) states.
+// Ids go straight to HBM, the fold rewrites the words already in registers,
+// and the last chunk to finish turns the per-table end offsets into counts.
+// ---------------------------------------------------------------------------
+constexpr int CF_THREADS = 256;
+constexpr int CF_WPT = 4;
+constexpr int CF_WPB = CF_THREADS * CF_WPT;  // 1024 words per chunk
+constexpr unsigned long long CF_AGG = 1ull << 62, CF_INC = 2ull << 62;
+constexpr unsigned long long CF_MASK31 = (1ull << 31) - 1;
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct CapFArgs {
+    uint32_t *interval;
+    uint32_t *baseline;  // may be null
+    int64_t *ids_int;
+    int64_t *ids_uni;
+    int64_t *counts;
+    unsigned long long *status;  // [nchunks]
+    unsigned long long *ends;    // [ntables] packed (uni << 31 | int) inclusive end offsets
+    unsigned int *ticket;        // [2]: ticket, done
+    int64_t word_off[DS_MAX_TABLES + 1];
+    int64_t chunk_off[DS_MAX_TABLES + 1];
+    int ntables;
+    int nchunks;
+    int fold;
+};
+
+__global__ void __launch_bounds__(CF_THREADS) capture_fused_kernel(const CapFArgs a) {
+    __shared__ int s_chunk;
+    __shared__ unsigned s_warp[CF_THREADS / 32];
+    __shared__ unsigned long long s_prefix;
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_chunk = (int)atomicAdd(a.ticket, 1u);
+    __syncthreads();
+    const int c = s_chunk;
+    int t = 0;
+    {
+        int lo = 0, hi = a.ntables - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (a.chunk_off[mid] <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        t = lo;
+    }
+    const int64_t wt0 = a.word_off[t];
+    const int64_t w0 = wt0 + (int64_t)(c - a.chunk_off[t]) * CF_WPB + threadIdx.x * CF_WPT;
+    const int64_t wend = a.word_off[t + 1];
+    uint32_t iv[CF_WPT], uv[CF_WPT];
+    unsigned ci = 0, cu = 0;
+#pragma unroll
+    for (int k = 0; k < CF_WPT; k++) {
+        int64_t w = w0 + k;
+        iv[k] = w < wend ? a.interval[w] : 0u;
+        uint32_t bv = (w < wend && a.baseline) ? a.baseline[w] : 0u;
+        uv[k] = iv[k] | bv;
+        ci += __popc(iv[k]);
+        cu += __popc(uv[k]);
+    }
+    // block exclusive scan of packed (cu << 16 | ci); totals <= 32768 each
+    unsigned p = ci | (cu << 16);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned x = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(DS_FULL_MASK, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    unsigned wbase = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < CF_THREADS / 32; k++) {
+        unsigned v = s_warp[k];
+        wbase += k < wid ? v : 0u;
+        total += v;
+    }
+    const unsigned excl = wbase + x - p;
+    // publish the aggregate, then look back for the exclusive prefix: warp 0
+    // inspects 32 predecessors per probe and stops at the nearest inclusive one
+    if (wid == 0) {
+        const unsigned long long agg = (unsigned long long)(total & 0xffffu) |
+                                       ((unsigned long long)(total >> 16) << 31);
+        unsigned long long pi = 0, pu = 0;
+        if (c == 0) {
+            if (lane == 0) st_release(a.status + c, CF_INC | agg);
+        } else {
+            if (lane == 0) st_release(a.status + c, CF_AGG | agg);
+            int q = c - 1 - lane;
+            while (true) {
+                // chunks before 0 count as an inclusive prefix of 0
+                unsigned long long s = q >= 0 ? ld_acquire(a.status + q) : CF_INC;
+                const unsigned flag = (unsigned)(s >> 62);
+                if (__any_sync(DS_FULL_MASK, flag == 0)) continue;  // not all published: re-probe
+                const unsigned inc = __ballot_sync(DS_FULL_MASK, flag == 2);
+                const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive (lowest lane)
+                unsigned long long vi = lane <= stop ? (s & CF_MASK31) : 0ull;
+                unsigned long long vu = lane <= stop ? ((s >> 31) & CF_MASK31) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    vi += __shfl_xor_sync(DS_FULL_MASK, vi, o);
+                    vu += __shfl_xor_sync(DS_FULL_MASK, vu, o);
+                }
+                pi += vi;
+                pu += vu;
+                if (inc) break;
+                q -= 32;
+            }
+            if (lane == 0) {
+                unsigned long long incl = (pi + (total & 0xffffu)) | ((pu + (total >> 16)) << 31);
+                st_release(a.status + c, CF_INC | incl);
+            }
+        }
+        if (lane == 0) {
+            const unsigned long long pre = pi | (pu << 31);
+            s_prefix = pre;
+            // end offset of a table = inclusive prefix of its last chunk
+            if (c == a.chunk_off[t + 1] - 1)
+                a.ends[t] = (pi + (total & 0xffffu)) | ((pu + (total >> 16)) << 31);
+        }
+    }
+    __syncthreads();
+    const unsigned long long pre = s_prefix;
+    int64_t oi = (int64_t)(pre & CF_MASK31) + (excl & 0xffffu);
+    int64_t ou = (int64_t)((pre >> 31) & CF_MASK31) + (excl >> 16);
+    const int64_t row0 = (w0 - wt0) * 32;
+#pragma unroll
+    for (int k = 0; k < CF_WPT; k++) {
+        if (a.ids_int) {
+            uint32_t m = iv[k];
+            while (m) {
+                int b = __ffs(m) - 1;
+                a.ids_int[oi++] = row0 + 32 * k + b;
+                m &= m - 1;
+            }
+        }
+        if (a.ids_uni) {
+            uint32_t m = uv[k];
+            while (m) {
+                int b = __ffs(m) - 1;
+                a.ids_uni[ou++] = row0 + 32 * k + b;
+                m &= m - 1;
+            }
+        }
+        int64_t w = w0 + k;
+        if (w < wend && a.fold) {  // reset_interval (1) / reset_baseline (2)
+            if (a.baseline) a.baseline[w] = a.fold == 1 ? uv[k] : 0u;
+            a.interval[w] = 0u;
+        }
+    }
+    // the last chunk to finish converts table end offsets into counts
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(a.ticket + 1, 1u) == (unsigned)a.nchunks - 1;
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        const int nt = a.ntables;
+        for (int k = threadIdx.x; k < nt; k += CF_THREADS) {
+            unsigned long long e = ld_acquire(a.ends + k);
+            unsigned long long b = k ? ld_acquire(a.ends + k - 1) : 0ull;
+            a.counts[k] = (int64_t)((e & CF_MASK31) - (b & CF_MASK31));
+            a.counts[nt + 1 + k] = (int64_t)(((e >> 31) & CF_MASK31) - ((b >> 31) & CF_MASK31));
+        }
+        if (threadIdx.x == 0) {
+            unsigned long long e = ld_acquire(a.ends + nt - 1);
+            a.counts[nt] = (int64_t)(e & CF_MASK31);
+            a.counts[2 * nt + 1] = (int64_t)((e >> 31) & CF_MASK31);
+        }
+    }
+}
+
 }  // namespace ds
 
 using namespace ds;
 
-extern "C" int ds_mark(uint32_t *words, const int64_t *word_off, const int64_t *rows,
-                       const int64_t *idx, const int64_t *seg_off_host,
-                       const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream) {
+static int mark_impl(uint32_t *words, const int64_t *word_off, const int64_t *rows,
+                     const void *idx, int idx32, const int64_t *seg_off_host,
+                     const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream) {
     if (nseg < 1 || nseg > DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark: nseg out of range");
     if (!words || !word_off || !rows || !flags) return host::fail(DS_ERR_ARG, "ds_mark: null pointer");
     MarkArgs a;
     a.words = words;
     a.idx = idx;
+    a.idx32 = idx32;
     a.flags = flags;
     a.nseg = nseg;
     for (int s = 0; s < nseg; s++) {
@@ -315,9 +777,81 @@ extern "C" int ds_mark(uint32_t *words, const int64_t *word_off, const int64_t *
     int64_t total = a.seg_off[nseg] - a.seg_off[0];
     if (total <= 0) return DS_OK;
     if (!idx) return host::fail(DS_ERR_ARG, "ds_mark: null idx");
-    int64_t blocks = host::grid_for(total, 256, 8);
-    mark_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a);
+    // one contiguous, 8-aligned range per CTA; exactly one wave of resident CTAs
+    const int64_t quantum = (int64_t)MARK_THREADS * MARK_PER_THREAD;
+    int per_sm = 0;
+    if (idx32)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mark_kernel<int32_t>, MARK_THREADS, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mark_kernel<int64_t>, MARK_THREADS, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = host::grid_for((total + MARK_PER_THREAD - 1) / MARK_PER_THREAD, MARK_THREADS,
+                                    per_sm);
+    int64_t per_block = (total + blocks - 1) / blocks;
+    per_block = (per_block + quantum - 1) / quantum * quantum;
+    blocks = (total + per_block - 1) / per_block;
+    const size_t isz = idx32 ? 4 : 8;
+    int vec = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) &&
+              ((a.seg_off[0] * (int64_t)isz) % 16 == 0);
+    int64_t max_word = 0;
+    for (int s = 0; s < nseg; s++) max_word = a.word_off[s] + (a.rows[s] + 31) / 32 > max_word
+                                                 ? a.word_off[s] + (a.rows[s] + 31) / 32 : max_word;
+    // word ids are 32-bit inside the kernel (and the cache keys are word+1)
+    if (max_word >= (int64_t)0xffffffffLL)
+        return host::fail(DS_ERR_CONFIG, "ds_mark: a table set holds at most 2^32-1 bitmap words");
+    int use_cache = 1;
+    // (the TMA kernel's cache keys are 31-bit word ids)
+    // every segment must start 16-byte aligned for the bulk copies
+    bool seg_aligned = true;
+    for (int s = 0; s <= nseg; s++) seg_aligned &= ((a.seg_off[s] * (int64_t)isz) % 16) == 0;
+    if (vec && seg_aligned && max_word < (int64_t)0x7fffffffLL && !host::env_flag("DS_MARK_NO_TMA")) {
+        // TMA-streamed form: CTAs never straddle a segment; each CTA's range
+        // is a multiple of a stage so every bulk copy starts 16-byte aligned
+        const int ids_per_stage = MK_STAGE_BYTES / (int)isz;
+        const size_t smem = (size_t)MK_STAGES * MK_STAGE_BYTES;
+        auto fn = idx32 ? (void (*)(const MarkArgs, int64_t, int))mark_tma_kernel<int32_t>
+                        : (void (*)(const MarkArgs, int64_t, int))mark_tma_kernel<int64_t>;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
+        int tper = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, fn, MARK_THREADS, smem);
+        if (tper < 1) tper = 1;
+        int64_t tb = (int64_t)host::sm_count() * tper;
+        int64_t pb = (total + tb - 1) / tb;
+        pb = (pb + ids_per_stage - 1) / ids_per_stage * ids_per_stage;
+        int64_t nb = 0;
+        for (int s = 0; s < nseg; s++) {
+            a.blk_off[s] = (int)nb;
+            int64_t len = a.seg_off[s + 1] - a.seg_off[s];
+            nb += (len + pb - 1) / pb;
+        }
+        a.blk_off[nseg] = (int)nb;
+        if (nb == 0) return DS_OK;
+        fn<<<(unsigned)nb, MARK_THREADS, smem, (cudaStream_t)stream>>>(a, pb, 0);
+        return host::check_launch("ds_mark");
+    }
+    if (idx32)
+        mark_kernel<int32_t><<<(unsigned)blocks, MARK_THREADS, 0, (cudaStream_t)stream>>>(
+            a, per_block, vec, use_cache);
+    else
+        mark_kernel<int64_t><<<(unsigned)blocks, MARK_THREADS, 0, (cudaStream_t)stream>>>(
+            a, per_block, vec, use_cache);
     return host::check_launch("ds_mark");
+}
+
+extern "C" int ds_mark(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+                       const int64_t *idx, const int64_t *seg_off_host,
+                       const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream) {
+    return mark_impl(words, word_off_host, rows_host, idx, 0, seg_off_host, seg_table_host, nseg,
+                     flags, stream);
+}
+
+extern "C" int ds_mark_i32(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+                           const int32_t *idx, const int64_t *seg_off_host,
+                           const int32_t *seg_table_host, int nseg, uint32_t *flags,
+                           void *stream) {
+    return mark_impl(words, word_off_host, rows_host, idx, 1, seg_off_host, seg_table_host, nseg,
+                     flags, stream);
 }
 
 extern "C" int ds_mark_table(uint32_t *words, int64_t rows, const int64_t *idx, int64_t n,
@@ -365,6 +899,37 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
     (void)rows_host;
     if (ntables < 1 || ntables > DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_capture: ntables");
     if (!interval || !counts || !workspace) return host::fail(DS_ERR_ARG, "ds_capture: null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t total_rows = 0;
+    for (int t = 0; t < ntables; t++) total_rows += (word_off_host[t + 1] - word_off_host[t]) * 32;
+    if (total_rows < (int64_t)CF_MASK31) {
+        // single-pass path (ids per scope fit the 31-bit look-back fields)
+        CapFArgs f;
+        f.interval = interval;
+        f.baseline = baseline;
+        f.ids_int = ids_int;
+        f.ids_uni = ids_union;
+        f.counts = counts;
+        f.ntables = ntables;
+        f.fold = fold;
+        int64_t nch = 0;
+        for (int t = 0; t <= ntables; t++) f.word_off[t] = word_off_host[t];
+        for (int t = 0; t < ntables; t++) {
+            f.chunk_off[t] = nch;
+            int64_t w = word_off_host[t + 1] - word_off_host[t];
+            nch += w > 0 ? (w + CF_WPB - 1) / CF_WPB : 1;
+        }
+        f.chunk_off[ntables] = nch;
+        f.nchunks = (int)nch;
+        size_t need = 16 + (size_t)(nch + ntables) * sizeof(unsigned long long);
+        if (workspace_bytes < need) return host::fail(DS_ERR_ARG, "ds_capture: workspace too small");
+        f.ticket = reinterpret_cast<unsigned int *>(workspace);
+        f.status = reinterpret_cast<unsigned long long *>(static_cast<char *>(workspace) + 16);
+        f.ends = f.status + nch;
+        cudaMemsetAsync(workspace, 0, 16 + (size_t)nch * sizeof(unsigned long long), s);
+        capture_fused_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
+        return host::check_launch("ds_capture");
+    }
     CapArgs a;
     a.interval = interval;
     a.baseline = baseline;
@@ -388,7 +953,6 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
     if (workspace_bytes < need) return host::fail(DS_ERR_ARG, "ds_capture: workspace too small");
     a.chunk_cnt = reinterpret_cast<unsigned long long *>(workspace);
     a.chunk_base = a.chunk_cnt + 2 * nch;
-    cudaStream_t s = (cudaStream_t)stream;
     capture_count_kernel<<<(unsigned)nch, CAP_THREADS, 0, s>>>(a);
     capture_scan_kernel<<<1, 1024, 0, s>>>(a);
     capture_write_kernel<<<(unsigned)nch, CAP_THREADS, 0, s>>>(a);

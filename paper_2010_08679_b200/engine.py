@@ -143,20 +143,22 @@ class ShardWriter:
         return int(sum(hdr + int(n) * rec for n in rows))
 
     def write(self, payload: torch.Tensor, ids: torch.Tensor | None = None,
-              counts: torch.Tensor | None = None, ids_offsets=None, stream=None) -> None:
+              counts: torch.Tensor | None = None, ids_offsets=None, *, local_ids: bool = False,
+              stream=None) -> None:
         """Launch layout + writer (+ error reduction).
 
-        Incremental when `ids` is given: ids is the concatenation of every
-        table's global row ids (ascending per table), counts a device int64
-        tensor of per-table lengths, ids_offsets the host start of each
-        table's ids (defaults to the exclusive prefix of the concatenation,
-        which is the layout capture() produces).
+        Incremental when `ids` is given: ids concatenates every table's row
+        ids (ascending per table) and counts is a device int64 tensor of
+        per-table lengths.  ids_offsets gives each table's start on the host;
+        None means "packed" -- the starts are the prefix sums of counts,
+        computed on the device (capture's layout, no host sync).  local_ids:
+        the ids are table-local rows (capture output) instead of global ids.
         """
         incremental = ids is not None
         self.params.incremental = int(incremental)
-        if incremental:
-            if ids_offsets is None:
-                raise ValueError("ids_offsets required for incremental writes")
+        self.params.ids_packed = int(incremental and ids_offsets is None)
+        self.params.ids_local = int(local_ids)
+        if incremental and ids_offsets is not None:
             for k in range(len(self.tables)):
                 self._descs[k].ids_off = int(ids_offsets[k])
         self.flags.zero_()

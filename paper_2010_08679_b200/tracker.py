@@ -260,11 +260,43 @@ class ModelTracker:
             rows_c = np.array([rows[t] for t in uniq], dtype=np.int64)
             tab_c = np.array([remap[t] for t in sub_t], dtype=np.int32)
             so = np.ascontiguousarray(seg_off[s0:s1 + 1])
-            _lib.check(L.ds_mark(self._ibuf.data_ptr(), wo_c.ctypes.data_as(ctypes.c_void_p),
+            fn = L.ds_mark_i32 if idx.dtype == torch.int32 else L.ds_mark
+            _lib.check(fn(self._ibuf.data_ptr(), wo_c.ctypes.data_as(ctypes.c_void_p),
                                  rows_c.ctypes.data_as(ctypes.c_void_p), idx.data_ptr(),
                                  so.ctypes.data_as(ctypes.c_void_p),
                                  tab_c.ctypes.data_as(ctypes.c_void_p), s1 - s0,
                                  self._flags.data_ptr(), stream), "mark_batch")
+
+    def capture_into(self, ids: torch.Tensor, counts: torch.Tensor, fold: int = 1,
+                     scope: str = "interval") -> None:
+        """K2 without any host synchronisation (the stall-window form).
+
+        Writes the chosen scope's local row ids of every table, concatenated in
+        table order, into `ids` (capacity >= total rows) and the per-table
+        counts into counts[:ntables] (counts[ntables] = total), then folds
+        (1: reset_interval, 2: reset_baseline, 0: none).  At most 64 tables.
+        """
+        if len(self._tids) > _lib.MAX_TABLES:
+            raise ValueError("capture_into supports at most 64 tables")
+        L = _lib.lib()
+        nt = len(self._tids)
+        if not hasattr(self, "_cap_ws"):
+            wo = np.array(self._word_off, dtype=np.int64)
+            rows = np.array([self._rows[t] for t in self._tids], dtype=np.int64)
+            ws_bytes = int(L.ds_capture_workspace_size(int(wo[-1]), nt))
+            self._cap_ws = (wo, rows, torch.empty(ws_bytes, dtype=torch.uint8, device=self.device))
+            self._cap_counts = torch.zeros(2 * nt + 2, dtype=torch.int64, device=self.device)
+        wo, rows, ws = self._cap_ws
+        union = scope != "interval"
+        cnt = self._cap_counts
+        _lib.check(L.ds_capture(self._ibuf.data_ptr(), self._bbuf.data_ptr(),
+                                wo.ctypes.data_as(ctypes.c_void_p),
+                                rows.ctypes.data_as(ctypes.c_void_p), nt,
+                                None if union else ids.data_ptr(),
+                                ids.data_ptr() if union else None, cnt.data_ptr(), fold,
+                                ws.data_ptr(), ws.numel(), _lib.stream_handle()), "capture_into")
+        src = cnt[nt + 1:2 * nt + 2] if union else cnt[:nt + 1]
+        counts[:nt + 1].copy_(src, non_blocking=True)
 
     def interval_bitmap(self, table_id: int) -> DirtyBitmap:
         return self._interval[table_id]
