@@ -169,7 +169,7 @@ typedef struct {
  *   sec_off[t]   byte offset of table t's section (header) in the payload,
  *   sec_off[ntables] total payload bytes,
  * and the tile schedule the writer uses.  Everything stays on device. */
-DS_API size_t ds_writer_workspace_size(int ntables, int64_t max_rows);
+DS_API size_t ds_writer_workspace_size(int ntables, int64_t max_rows, int64_t dim);
 DS_API int ds_write_payload(const ds_table_desc *tables_host, int ntables, const ds_ckpt_params *p,
                      const int64_t *ids, const int64_t *counts, uint8_t *payload,
                      int64_t payload_capacity, int64_t *sec_off, double *err_sum,

@@ -86,7 +86,7 @@ _SIGNATURES = {
     "ds_popcount": (_I, [_P, _I64, _P, _P]),
     "ds_capture_workspace_size": (_SZ, [_I64, _I]),
     "ds_capture": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _I, _P, _SZ, _P]),
-    "ds_writer_workspace_size": (_SZ, [_I, _I64]),
+    "ds_writer_workspace_size": (_SZ, [_I, _I64, _I64]),
     "ds_write_payload": (_I, [_P, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
     "ds_record_size": (_I64, [_I64, _I, _I, _I]),
     "ds_restore_section": (_I, [_P, _I64, _I64, _I, _I, _I, _I64, _I64, _I64, _P, _I64, _P, _P,

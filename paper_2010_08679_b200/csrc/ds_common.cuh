@@ -66,6 +66,18 @@ __device__ __forceinline__ int grp_or(int v) {
 template <int G>
 constexpr int log2i() { return G <= 1 ? 0 : 1 + log2i<G / 2>(); }
 
+// min/max that return NaN when either input is NaN (PTX .NaN, sm_80+)
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // element layout
 // ---------------------------------------------------------------------------
@@ -166,8 +178,10 @@ __device__ __forceinline__ RowQ make_rowq(float lo, float hi, int L, double y = 
         r.mode = 2;
     } else {
         r.mode = 0;
-        r.inv = __fdiv_rn((float)L, rng);
-        // |v_fast - v_ref| <= 5u*L (c-lo, rng, div, mul roundings); 8u*L margin
+        // inv = L/rng via a correctly rounded reciprocal and one product:
+        // rel. error <= 3u (rng, rcp, mul); with c-lo and v = t*inv that is
+        // |v_fast - v_ref| <= 5u*L, covered by the 8u*L guard band
+        r.inv = __fmul_rn(__frcp_rn(rng), (float)L);
         r.eps = 8.f * kU * (float)L;
     }
     return r;

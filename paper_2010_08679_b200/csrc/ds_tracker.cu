@@ -283,11 +283,20 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a
             for (int q = 0; q < PER_THREAD * (int)sizeof(IdxT) / 16; q++)
                 reinterpret_cast<int4 *>(v)[q] = reinterpret_cast<const int4 *>(b + j0)[q];
             if (small) {
+                // read first: hot words are already set and same-address reads
+                // broadcast, while same-address shared atomics serialise
+                uint32_t cur[PER_THREAD];
+                bool ok[PER_THREAD];
 #pragma unroll
                 for (int q = 0; q < PER_THREAD; q++) {
-                    const bool ok = (uint64_t)(int64_t)v[q] < rows;  // negatives wrap high
-                    bad |= !ok;
-                    if (ok) atomicOr(win + ((uint32_t)v[q] >> 5), 1u << ((uint32_t)v[q] & 31));
+                    ok[q] = (uint64_t)(int64_t)v[q] < rows;  // negatives wrap high
+                    bad |= !ok[q];
+                    cur[q] = ok[q] ? win[(uint32_t)v[q] >> 5] : ~0u;
+                }
+#pragma unroll
+                for (int q = 0; q < PER_THREAD; q++) {
+                    const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
+                    if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
                 }
             } else {
                 // all cache probes before any update so their latencies overlap
@@ -750,6 +759,201 @@ __global__ void __launch_bounds__(CF_THREADS) capture_fused_kernel(const CapFArg
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// K2 as count -> scan -> emit over chunks of 1024 words (4 consecutive words
+// per thread).  The emit pass knows every chunk's base, so no CTA waits on
+// another (the look-back form above serialises through chunk order).
+// 4 consecutive words per thread: chunks of 1024 words (32768 rows) keep the
+// per-CTA emission short and balanced
+// ---------------------------------------------------------------------------
+constexpr int C3_WPT = 4;
+constexpr int C3_WPB = CF_THREADS * C3_WPT;
+
+struct Cap3Args {
+    uint32_t *interval;
+    uint32_t *baseline;  // may be null
+    int64_t *ids_int;
+    int64_t *ids_uni;
+    int64_t *counts;
+    unsigned long long *cnt;   // [nchunks] packed (union << 32 | interval)
+    unsigned long long *base;  // [nchunks] exclusive prefix, same packing
+    int64_t word_off[DS_MAX_TABLES + 1];
+    int64_t chunk_off[DS_MAX_TABLES + 1];
+    int ntables;
+    int nchunks;
+    int fold;
+};
+
+__device__ __forceinline__ int cap3_table(const Cap3Args &a, int c) {
+    int t = 0;
+    while (t + 1 < a.ntables && a.chunk_off[t + 1] <= c) t++;
+    return t;
+}
+
+__device__ __forceinline__ void cap3_load(const Cap3Args &a, int c, int t, uint32_t (&iv)[C3_WPT],
+                                          uint32_t (&uv)[C3_WPT], int64_t &w0, int64_t &wend) {
+    w0 = a.word_off[t] + (int64_t)(c - a.chunk_off[t]) * C3_WPB + threadIdx.x * C3_WPT;
+    wend = a.word_off[t + 1];
+#pragma unroll
+    for (int k = 0; k < C3_WPT; k++) {
+        const int64_t w = w0 + k;
+        iv[k] = w < wend ? __ldcg(a.interval + w) : 0u;
+        const uint32_t bv = (w < wend && a.baseline) ? __ldcg(a.baseline + w) : 0u;
+        uv[k] = iv[k] | bv;
+    }
+}
+
+__global__ void __launch_bounds__(CF_THREADS) cap3_count_kernel(const Cap3Args a) {
+    __shared__ unsigned long long s_w[CF_THREADS / 32];
+    const int c = blockIdx.x, t = cap3_table(a, c);
+    uint32_t iv[C3_WPT], uv[C3_WPT];
+    int64_t w0, wend;
+    cap3_load(a, c, t, iv, uv, w0, wend);
+    unsigned long long v = 0;
+#pragma unroll
+    for (int k = 0; k < C3_WPT; k++)
+        v += (unsigned long long)__popc(iv[k]) | ((unsigned long long)__popc(uv[k]) << 32);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(DS_FULL_MASK, v, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int k = 0; k < CF_THREADS / 32; k++) s += s_w[k];
+        a.cnt[c] = s;
+    }
+}
+
+// one CTA: exclusive scan of the packed chunk counts, per-table counts
+__global__ void __launch_bounds__(1024) cap3_scan_kernel(const Cap3Args a) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < a.nchunks; s0 += 1024) {
+        const int i = s0 + threadIdx.x;
+        const unsigned long long v = i < a.nchunks ? a.cnt[i] : 0ull;
+        unsigned long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long wv = s_w[lane], wx = wv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long y = __shfl_up_sync(DS_FULL_MASK, wx, o);
+                if (lane >= o) wx += y;
+            }
+            s_w[lane] = wx - wv;
+        }
+        __syncthreads();
+        const unsigned long long carry = s_carry;
+        if (i < a.nchunks) a.base[i] = carry + s_w[wid] + x - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = carry + s_w[wid] + x;
+        __syncthreads();
+    }
+    const unsigned long long total = s_carry;
+    const int nt = a.ntables;
+    for (int t = threadIdx.x; t < nt; t += 1024) {
+        const int c0 = (int)a.chunk_off[t], c1 = (int)a.chunk_off[t + 1];
+        const unsigned long long b0 = c0 < a.nchunks ? a.base[c0] : total;
+        const unsigned long long b1 = c1 < a.nchunks ? a.base[c1] : total;
+        a.counts[t] = (int64_t)((uint32_t)b1 - (uint32_t)b0);
+        a.counts[nt + 1 + t] = (int64_t)((b1 >> 32) - (b0 >> 32));
+    }
+    if (threadIdx.x == 0) {
+        a.counts[nt] = (int64_t)(uint32_t)total;
+        a.counts[2 * nt + 1] = (int64_t)(total >> 32);
+    }
+}
+
+constexpr unsigned CAP3_STAGE = 8192;  // ids staged per scope and chunk (32 KB)
+
+__global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a) {
+    __shared__ unsigned long long s_warp[CF_THREADS / 32];
+    __shared__ uint32_t s_ids[CAP3_STAGE];
+    const int c = blockIdx.x, t = cap3_table(a, c);
+    uint32_t iv[C3_WPT], uv[C3_WPT];
+    int64_t w0, wend;
+    cap3_load(a, c, t, iv, uv, w0, wend);
+    unsigned ci = 0, cu = 0;
+#pragma unroll
+    for (int k = 0; k < C3_WPT; k++) {
+        ci += __popc(iv[k]);
+        cu += __popc(uv[k]);
+    }
+    // block exclusive scan of packed (cu << 32 | ci)
+    const unsigned long long p = (unsigned long long)ci | ((unsigned long long)cu << 32);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned long long x = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    unsigned long long wbase = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < CF_THREADS / 32; k++) {
+        wbase += k < wid ? s_warp[k] : 0ull;
+        tot += s_warp[k];
+    }
+    const unsigned long long excl = wbase + x - p;
+    const unsigned long long b = a.base[c];
+    // ids are staged in shared memory as chunk-local row offsets and
+    // leave as coalesced int64 runs; a chunk denser than the stage writes
+    // straight from the registers
+    const int64_t crow0 = (w0 - threadIdx.x * C3_WPT - a.word_off[t]) * 32;  // chunk's first row
+    const unsigned lrow0 = threadIdx.x * C3_WPT * 32;                         // thread's first row
+    for (int scope = 0; scope < 2; scope++) {
+        int64_t *out = scope ? a.ids_uni : a.ids_int;
+        if (!out) continue;
+        const unsigned n = (unsigned)(scope ? tot >> 32 : tot & 0xffffffffu);
+        unsigned o = (unsigned)(scope ? excl >> 32 : excl & 0xffffffffu);
+        const int64_t gbase = scope ? (int64_t)(b >> 32) : (int64_t)(uint32_t)b;
+        if (n <= CAP3_STAGE) {
+#pragma unroll
+            for (int k = 0; k < C3_WPT; k++) {
+                uint32_t m = scope ? uv[k] : iv[k];
+                while (m) {
+                    s_ids[o++] = lrow0 + 32 * k + __ffs(m) - 1;
+                    m &= m - 1;
+                }
+            }
+            __syncthreads();
+            for (unsigned j = threadIdx.x; j < n; j += CF_THREADS)
+                __stcs(out + gbase + j, crow0 + s_ids[j]);
+            __syncthreads();
+        } else {
+            int64_t oo = gbase + o;
+#pragma unroll
+            for (int k = 0; k < C3_WPT; k++) {
+                uint32_t m = scope ? uv[k] : iv[k];
+                while (m) {
+                    out[oo++] = crow0 + lrow0 + 32 * k + __ffs(m) - 1;
+                    m &= m - 1;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < C3_WPT; k++) {
+        const int64_t w = w0 + k;
+        if (w < wend && a.fold) {  // reset_interval (1) / reset_baseline (2)
+            if (a.baseline) a.baseline[w] = a.fold == 1 ? uv[k] : 0u;
+            a.interval[w] = 0u;
+        }
+    }
+}
+
 }  // namespace ds
 
 using namespace ds;
@@ -902,6 +1106,34 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     int64_t total_rows = 0;
     for (int t = 0; t < ntables; t++) total_rows += (word_off_host[t + 1] - word_off_host[t]) * 32;
+    if (total_rows < (int64_t)0xffffffffLL && !host::env_flag("DS_CAPTURE_LOOKBACK")) {
+        // count -> scan -> emit (ids per scope fit the 32-bit packed counts)
+        Cap3Args f;
+        f.interval = interval;
+        f.baseline = baseline;
+        f.ids_int = ids_int;
+        f.ids_uni = ids_union;
+        f.counts = counts;
+        f.ntables = ntables;
+        f.fold = fold;
+        int64_t nch = 0;
+        for (int t = 0; t <= ntables; t++) f.word_off[t] = word_off_host[t];
+        for (int t = 0; t < ntables; t++) {
+            f.chunk_off[t] = nch;
+            int64_t w = word_off_host[t + 1] - word_off_host[t];
+            nch += w > 0 ? (w + C3_WPB - 1) / C3_WPB : 1;
+        }
+        f.chunk_off[ntables] = nch;
+        f.nchunks = (int)nch;
+        size_t need = 2 * (size_t)nch * sizeof(unsigned long long);
+        if (workspace_bytes < need) return host::fail(DS_ERR_ARG, "ds_capture: workspace too small");
+        f.cnt = reinterpret_cast<unsigned long long *>(workspace);
+        f.base = f.cnt + nch;
+        cap3_count_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
+        cap3_scan_kernel<<<1, 1024, 0, s>>>(f);
+        cap3_emit_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
+        return host::check_launch("ds_capture");
+    }
     if (total_rows < (int64_t)CF_MASK31) {
         // single-pass path (ids per scope fit the 31-bit look-back fields)
         CapFArgs f;

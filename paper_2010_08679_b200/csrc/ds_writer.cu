@@ -43,12 +43,21 @@ __global__ void layout_kernel(const WriterArgs a) {
     if (off > a.capacity) atomicOr(a.flags, DS_FLAG_CAPACITY);
 }
 
-__global__ void err_reduce_kernel(const double *partials, int n, double *out) {
+// deterministic final error sum: writer CTAs in order, then fixup CTAs
+__global__ void err_reduce_kernel(const double *partials, int n, const double *partials_fix,
+                                  int nfix, double *out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int i = 0; i < n; i++) s += partials[i];
+        for (int i = 0; i < nfix; i++) s += partials_fix[i];
         *out = s;
     }
+}
+
+// warp-tiles of the MODE 0/1 writer for `rows` records of dim `dim`
+static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
+    const int rpw = 32 / pick_cfg((int)dim, dim % 4 == 0).G;
+    return rows / rpw + ntables + 1;
 }
 
 }  // namespace ds
@@ -63,9 +72,14 @@ extern "C" int64_t ds_record_size(int64_t dim, int bitwidth, int aux, int increm
     return s;
 }
 
-extern "C" size_t ds_writer_workspace_size(int ntables, int64_t max_rows) {
-    (void)max_rows;
-    return (size_t)(3 * DS_MAX_TABLES + 4) * sizeof(int64_t) + (size_t)4096 * sizeof(double) + 256;
+static size_t ws_head_bytes() {
+    return (size_t)(3 * DS_MAX_TABLES + 4) * sizeof(int64_t) + (size_t)2 * 4096 * sizeof(double);
+}
+
+extern "C" size_t ds_writer_workspace_size(int ntables, int64_t max_rows, int64_t dim) {
+    // schedule + 2 x 4096 error partials + one fixup mask word per warp-tile
+    int64_t tiles = warp_tiles(max_rows > 0 ? max_rows : 0, ntables, dim > 0 ? dim : 1);
+    return ws_head_bytes() + (size_t)tiles * sizeof(uint32_t) + 256;
 }
 
 extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
@@ -77,7 +91,9 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         return host::fail(DS_ERR_ARG, "ds_write_payload: ntables out of range (1..64)");
     if (!p || !tables_host || !sec_off || !flags || !workspace || !payload)
         return host::fail(DS_ERR_ARG, "ds_write_payload: null pointer");
-    if (workspace_bytes < ds_writer_workspace_size(ntables, 0))
+    int64_t rows_bound = 0;
+    for (int t = 0; t < ntables; t++) rows_bound += tables_host[t].rows;
+    if (workspace_bytes < ds_writer_workspace_size(ntables, rows_bound, tables_host[0].dim))
         return host::fail(DS_ERR_ARG, "ds_write_payload: workspace too small");
     const int bw = p->bitwidth;
     if (!(bw == 0 || bw == 2 || bw == 3 || bw == 4 || bw == 8))
@@ -118,6 +134,8 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     a.counts = p->incremental ? counts : nullptr;
     a.sched = reinterpret_cast<int64_t *>(workspace);
     a.partials = reinterpret_cast<double *>(a.sched + 3 * DS_MAX_TABLES + 4);
+    a.partials_fix = a.partials + 4096;
+    a.fix_mask = reinterpret_cast<uint32_t *>(a.partials_fix + 4096);
     a.ids_packed = p->ids_packed;
     a.ids_local = p->ids_local;
     a.sec_off = sec_off;
@@ -135,24 +153,23 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     else fn = select_writer_mode2(c, pad);
     if (!fn) return host::fail(DS_ERR_CONFIG, "ds_write_payload: no kernel for this dim");
 
-    const int rpp = WT / c.G;
-    // MODE 0/1: a tile is ~32 KB of gathered rows (a multiple of the rows per
-    // pass); MODE 2: one pass per tile (compute-bound)
-    int tr = rpp;
+    int tr;
+    size_t smem;
     if (mode != 2) {
-        tr = (int)((16 * 1024) / ((int64_t)d * 4));  // 16 KB of rows per buffer (x2)
-        tr = tr / rpp * rpp;
-        if (tr < rpp) tr = rpp;
-        if (tr > 1024) tr = 1024;
+        // warp pipeline: tiles of 32/G records, per-warp stage + codes + 2 row
+        // buffers + 3 id buffers (writer_warp_kernel computes the same layout)
+        const int rpw = 32 / c.G;
+        tr = rpw;
+        const size_t warp_b = (size_t)align16(rpw * a.rec) + 16 + align16(rpw * d) +
+                              2 * (size_t)align16(rpw * d * 4) + 3 * (size_t)rpw * 8;
+        smem = warp_b * (WT / 32) + 16;  // + alignment slack
+    } else {
+        const int rpp = WT / c.G;  // one pass of rows per tile (compute-bound)
+        tr = rpp;
+        smem = (size_t)align16(tr * a.rec) + 16 + align16(rpp * d) +
+               (size_t)rpp * (d + 8) * sizeof(double);
     }
-    // keep the record stage within 48 KB
-    while (tr > rpp && (int64_t)tr * a.rec > 48 * 1024) tr -= rpp;
     a.tile_rows = tr;
-    size_t stage_bytes = (((size_t)tr * a.rec + 15) & ~(size_t)15) + 16;
-    size_t codes_bytes = ((size_t)rpp * d + 15) & ~(size_t)15;
-    size_t tail_bytes = mode == 2 ? (size_t)rpp * (d + 8) * sizeof(double)
-                                  : 2 * (((size_t)tr * d * 4 + 15) & ~(size_t)15) + 3 * (size_t)tr * 8;
-    size_t smem = stage_bytes + codes_bytes + tail_bytes;
     if (smem > 200 * 1024) return host::fail(DS_ERR_CONFIG, "ds_write_payload: record too large");
 
     // grid: persistent over an upper bound of the tile count
@@ -176,6 +193,7 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     fn<<<(unsigned)grid, WT, smem, s>>>(a);
     int st = host::check_launch("ds_write_payload");
     if (st) return st;
-    if (err_sum) err_reduce_kernel<<<1, 32, 0, s>>>(a.partials, (int)grid, err_sum);
+    int nfix = 0;
+    if (err_sum) err_reduce_kernel<<<1, 32, 0, s>>>(a.partials, (int)grid, a.partials_fix, nfix, err_sum);
     return host::check_launch("ds_write_payload(err)");
 }

@@ -50,6 +50,8 @@ struct WriterArgs {
     uint8_t *payload;
     int64_t capacity;
     double *partials;
+    double *partials_fix;  // per-CTA error of the rows re-coded by the fixup pass
+    uint32_t *fix_mask;    // MODE 1: per warp-tile mask of rows for the fixup pass
     uint32_t *flags;
     unsigned long long *stats;
 };
@@ -73,35 +75,37 @@ __device__ __forceinline__ uint32_t ld_u32_unaligned(const uint8_t *base, int o)
 
 // stream nbytes of the stage to dst (any alignment) with aligned 32-bit stores
 __device__ __forceinline__ void copy_out(uint8_t *__restrict__ dst, const uint8_t *stage,
-                                         int64_t nbytes) {
+                                         int64_t nbytes, int tid, int nthr) {
     // the stage is 16-byte aligned: an 8/16-byte aligned destination copies
     // with 64/128-bit moves (records of a tile are contiguous)
     const uintptr_t al = reinterpret_cast<uintptr_t>(dst);
     if ((al & 7) == 0) {
+        // (a tile stage is < 2^31 bytes: 32-bit induction variables)
+        const int nb = (int)nbytes;
         if ((al & 15) == 0) {
-            const int64_t n16 = nbytes >> 4;
-            for (int64_t k = threadIdx.x; k < n16; k += blockDim.x)
+            const int n16 = nb >> 4;
+            for (int k = tid; k < n16; k += nthr)
                 __stcs(reinterpret_cast<int4 *>(dst) + k, reinterpret_cast<const int4 *>(stage)[k]);
-            for (int64_t b = (n16 << 4) + threadIdx.x; b < nbytes; b += blockDim.x) dst[b] = stage[b];
+            for (int b = (n16 << 4) + tid; b < nb; b += nthr) dst[b] = stage[b];
         } else {
-            const int64_t n8 = nbytes >> 3;
-            for (int64_t k = threadIdx.x; k < n8; k += blockDim.x)
+            const int n8 = nb >> 3;
+            for (int k = tid; k < n8; k += nthr)
                 __stcs(reinterpret_cast<unsigned long long *>(dst) + k,
                        reinterpret_cast<const unsigned long long *>(stage)[k]);
-            for (int64_t b = (n8 << 3) + threadIdx.x; b < nbytes; b += blockDim.x) dst[b] = stage[b];
+            for (int b = (n8 << 3) + tid; b < nb; b += nthr) dst[b] = stage[b];
         }
         return;
     }
     int head = (int)((4 - (reinterpret_cast<uintptr_t>(dst) & 3)) & 3);
     if (head > nbytes) head = (int)nbytes;
-    if ((int)threadIdx.x < head) dst[threadIdx.x] = stage[threadIdx.x];
+    if ((int)tid < head) dst[tid] = stage[tid];
     int64_t nw = (nbytes - head) >> 2;
     uint32_t *dw = reinterpret_cast<uint32_t *>(dst + head);
-    for (int64_t k = threadIdx.x; k < nw; k += blockDim.x)
+    for (int64_t k = tid; k < nw; k += nthr)
         __stcs(dw + k, ld_u32_unaligned(stage, head + 4 * (int)k));  // streamed, not re-read
     int64_t done = head + 4 * nw;
     int tail = (int)(nbytes - done);
-    if ((int)threadIdx.x < tail) dst[done + threadIdx.x] = stage[done + threadIdx.x];
+    if ((int)tid < tail) dst[done + tid] = stage[done + tid];
 }
 
 // ---------------------------------------------------------------------------
@@ -133,350 +137,191 @@ __device__ __forceinline__ void cp_async_wait() {
 // ---------------------------------------------------------------------------
 // MODE 0: fp32 section (payload.py:101), 1: naive ranges (engine.py:163-164),
 // 2: greedy ranges (engine.py:166 -> quant.py:160-209).
-//
-// MODE 0/1 are HBM-bound gathers: per tile, (A) the tile's row ids go to
-// shared memory with coalesced loads, (B) every row of the tile is requested
-// with cp.async into shared memory (each lane copies the chunks it will later
-// code), (C) rows are coded from shared memory into the record stage, (D) the
-// stage streams out.  MODE 2 is compute-bound (~20 candidate evaluations per
-// row) and loads each row straight into registers.
-template <int G, int C, int VEC, int MODE, bool PAD>
-__global__ void __launch_bounds__(WT, MODE == 2 ? 1 : 4) writer_kernel(const WriterArgs a) {
-    using Lay = Layout<G, C, VEC>;
-    constexpr int EPL = C * VEC;
-    constexpr int RPP = WT / G;  // rows per pass
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int TR = a.tile_rows;
-    // without padding the layout covers the row exactly: dim is a constant
-    const int d = PAD ? a.dim : (VEC == 4 ? 4 * G * C : G * C);
-    // shared memory carve-up (host computes the same sizes)
-    const int stage_bytes = ((TR * a.rec + 15) & ~15) + 16;
-    uint8_t *stage = smem;
-    uint8_t *codes_sh = smem + stage_bytes;                        // RPP * d bytes
-    uint8_t *after_codes = codes_sh + ((RPP * d + 15) & ~15);
-    double *exact_sh = reinterpret_cast<double *>(after_codes);    // MODE 2: RPP*(d+8)
-    float *rows_sh = reinterpret_cast<float *>(after_codes);       // MODE 0/1: 2 x TR*d
-    int64_t *ids_sh =                                               // MODE 0/1: 3 x TR
-        reinterpret_cast<int64_t *>(after_codes + 2 * (((size_t)TR * d * 4 + 15) & ~(size_t)15));
 
-    __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
-    __shared__ double s_red[WT / 32];
-    const int nt = a.ntables;
-    for (int k = threadIdx.x; k < 3 * nt + 1; k += WT) s_sched[k] = a.sched[k];
-    __syncthreads();
-    if (a.sec_off[nt] > a.capacity) return;  // flagged by the layout kernel
-
-    const int lane = threadIdx.x & 31;
-    const int lig = lane & (G - 1);
-    const int slot = threadIdx.x / G;
-    const int L = a.L;
-    const int64_t total_tiles = s_sched[nt];
-    double err_acc = 0.0;
+// per-thread accumulators of the writer
+struct WAcc {
+    double err = 0.0;  // sum of row L2 errors (engine.py:171-173)
     unsigned n_exact_dec = 0, n_exact_codes = 0, n_rows = 0;
     bool bad_data = false, bad_ids = false;
+};
 
-    // tile k of this CTA -> (table, first record, records).  The table is the
-    // last one whose first tile is <= tile: one ballot per 32 tables.
-    auto tile_info = [&](int k, int &t, int64_t &i0, int &nrow) -> bool {
-        const int64_t tile = blockIdx.x + (int64_t)k * gridDim.x;
-        if (tile >= total_tiles) return false;
-        t = 0;
-        for (int b = 0; b < nt; b += 32) {
-            unsigned m = __ballot_sync(DS_FULL_MASK, b + lane < nt && s_sched[b + lane] <= tile);
-            if (m) t = b + 31 - __clz(m);
+// Code one row held by the G lanes of a group into its record in `rec`
+// (wire layout of payload.py:84-104): [u64 row] [f32 lo, f32 hi, codes] |
+// [dim f32] [dim f32 aux].  `cs` is the group's dim-byte code scratch,
+// `buf` its exact-evaluation scratch (MODE 2).
+template <int G, int C, int VEC, int MODE, bool PAD>
+__device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_desc &td,
+                                         float (&x)[C * VEC], const float *xs, bool valid, int64_t local,
+                                         uint8_t *rec, uint8_t *cs, double *buf, int lig, int d,
+                                         WAcc &acc) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    const int L = a.L;
+    const int64_t gid = td.row_base + local;
+    bool fix = false;  // MODE 1: row left to the exact fixup pass (fix_tile)
+    if (valid && a.incremental && lig == 0) {
+        if ((reinterpret_cast<uintptr_t>(rec) & 7) == 0)
+            *reinterpret_cast<uint64_t *>(rec) = (uint64_t)gid;
+        else
+            st_bytes(rec, (uint64_t)gid, 8);
+    }
+    if (MODE == 0) {
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < EPL; k++) {
+                int e = Lay::elem(lig, k);
+                if (e < d) st_u32(rec + a.par_off + 4 * e, __float_as_uint(x[k]));
+            }
         }
-        i0 = (tile - s_sched[t]) * TR;
-        nrow = (int)min((int64_t)TR, s_sched[nt + 1 + t] - i0);
-        return true;
-    };
-    // table-local row of a record (-1: outside the table -> BoundsError)
-    auto local_of = [&](const ds_table_desc &td, int64_t raw) -> int64_t {
-        // ids from capture are table-local; plan ids are global
-        int64_t local = a.ids_local ? raw : raw - td.row_base;
-        return (local < 0 || local >= td.rows) ? -1 : local;
-    };
-    // MODE 0/1 pipeline: ids of tile k+2 and rows of tile k+1 are in flight
-    // (cp.async groups) while tile k is coded
-    auto issue_ids = [&](int k) {
-        int t, nrow;
-        int64_t i0;
-        if (a.incremental && tile_info(k, t, i0, nrow)) {
-            const int64_t *src = a.ids + s_sched[2 * nt + 1 + t] + i0;
-            int64_t *dst = ids_sh + (size_t)(k % 3) * TR;
-            for (int j = threadIdx.x; j < nrow; j += WT) cp_async8(dst + j, src + j);
+    } else {
+        // finiteness (quant.py:70-72,173): x*0 is NaN exactly for NaN/Inf;
+        // naive range: row min / max (engine.py:163-164)
+        // (NaN-propagating min/max: a NaN or Inf element leaves lo or hi
+        // non-finite, so the range doubles as the finiteness test)
+        float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            if (!PAD || Lay::elem(lig, k) < d) {
+                mn = fmin_nan(mn, x[k]);
+                mx = fmax_nan(mx, x[k]);
+            }
         }
-        cp_async_commit();
-    };
-    auto issue_rows = [&](int k) {
-        int t, nrow;
-        int64_t i0;
-        if (tile_info(k, t, i0, nrow)) {
-            const ds_table_desc &td = a.t[t];
-            const int64_t *ids = ids_sh + (size_t)(k % 3) * TR;
-            float *rows = rows_sh + (size_t)(k & 1) * TR * d;
-            for (int r = slot; r < nrow; r += RPP) {
-                const int64_t local = a.incremental ? local_of(td, ids[r]) : i0 + r;
-                if (local < 0) continue;
-                const float *src = td.values + local * td.ld;
-                float *dst = rows + r * d;
-                // each lane requests exactly the chunks it will code
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            mn = fmin_nan(mn, __shfl_xor_sync(DS_FULL_MASK, mn, o, G));
+            mx = fmax_nan(mx, __shfl_xor_sync(DS_FULL_MASK, mx, o, G));
+        }
+        const bool fin = isfinite(mn) && isfinite(mx);
+        if (valid && !fin) acc.bad_data = true;
+        const bool row_ok = valid && fin;
+        float lo = mn, hi = mx;
+        if (!row_ok) { lo = 0.f; hi = 0.f; }
+        if (MODE == 2)
+            greedy_row<G, C, VEC, PAD>(x, d, lig, row_ok, lo, hi, L, a.bins, a.steps, buf, lo, hi,
+                                       acc.n_exact_dec, acc.n_exact_codes);
+        const RowQ rq = make_rowq(lo, hi, L, a.invL);
+        int q[EPL];
+        double sse = 0.0;
+        if (MODE == 1) {
+            // min/max ranges hold every element: no clip, v in [0, L(1+5u)].
+            // Round half to even through the 1.5*2^23 magic: the sum's low
+            // mantissa bits are the integer code, the difference its float.
+            // A row with a code inside the guard band of a tie (~0.3% of rows)
+            // or a range outside fp32's comfort zone is left to
+            // the fixup pass (fix_tile), which re-codes it in exact f64: no f64 code
+            // path here, so the hot loop keeps its registers.
+            float dev = 0.f;
+#pragma unroll
+            for (int k = 0; k < EPL; k++) {
+                const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
+                const float qm = __fadd_rn(v, 12582912.0f);
+                q[k] = __float_as_int(qm) & 0x3fffff;
+                const float qf = __fsub_rn(qm, 12582912.0f);
+                dev = fmaxf(dev, fabsf(__fsub_rn(v, qf)));
+                // err_sum term (engine.py:171-173): exact dequantized value
+                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf), (double)lo));
+                const double er = __dsub_rn((double)x[k], (double)dq);
+                if (!PAD || Lay::elem(lig, k) < d) sse = fma(er, er, sse);
+            }
+            dev = grp_max<G>(dev);  // every lane shuffles (no short-circuit)
+            fix = row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps);
+            if (rq.mode == 2) sse = 0.0;  // fix_tile adds this row's exact error
+        } else {
+#pragma unroll
+            for (int k = 0; k < EPL; k++) {
+                q[k] = code_of(x[k], rq, acc.n_exact_codes);
+                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)q[k]), (double)lo));
+                const double er = __dsub_rn((double)x[k], (double)dq);
+                if (!PAD || Lay::elem(lig, k) < d) sse = fma(er, er, sse);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < EPL; k++)
+            if (!row_ok || (PAD && Lay::elem(lig, k) >= d)) q[k] = 0;  // padding codes are 0
+        if (!row_ok) sse = 0.0;  // rejected rows add no error
+        sse = grp_sumd<G>(sse);
+        if (row_ok && lig == 0) {
+            // row L2 norm: sqrt as sse * rsqrt(sse) (within an ulp; err_sum is a
+            // diagnostic sum whose low bits depend on summation order anyway)
+            acc.err += sse > 0.0 ? sse * rsqrt(sse) : 0.0;
+            acc.n_rows++;
+            st_u32(rec + a.par_off, __float_as_uint(lo));
+            st_u32(rec + a.par_off + 4, __float_as_uint(hi));
+        }
+        // ---- pack (quant.py:376-382): LSB-first bitstream ----
+        uint8_t *pk = rec + a.code_off;
+        if (VEC == 4 && (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2)) {
+            if (valid) {
 #pragma unroll
                 for (int c = 0; c < C; c++) {
-                    if (VEC == 4) {
-                        int e = 4 * (lig + c * G);
-                        if (e < d) cp_async16(dst + e, src + e);
-                    } else {
-                        int e = lig + c * G;
-                        if (e < d) cp_async4(dst + e, src + e);
+                    int m = lig + c * G;  // chunk index: elements 4m..4m+3
+                    if (4 * m < d) {
+                        uint32_t v;
+                        if (a.bitwidth == 8) {
+                            v = q[4 * c] | (q[4 * c + 1] << 8) | (q[4 * c + 2] << 16) |
+                                ((uint32_t)q[4 * c + 3] << 24);
+                            st_u32(pk + 4 * m, v);
+                        } else if (a.bitwidth == 4) {
+                            v = q[4 * c] | (q[4 * c + 1] << 4) | (q[4 * c + 2] << 8) |
+                                (q[4 * c + 3] << 12);
+                            st_bytes(pk + 2 * m, v, 2);
+                        } else {
+                            v = q[4 * c] | (q[4 * c + 1] << 2) | (q[4 * c + 2] << 4) |
+                                (q[4 * c + 3] << 6);
+                            pk[m] = (uint8_t)v;
+                        }
                     }
                 }
             }
-        }
-        cp_async_commit();
-    };
-    if (MODE != 2) {  // prologue: ids(0) landed, then ids(1) and rows(0) in flight
-        issue_ids(0);
-        cp_async_wait<0>();
-        __syncthreads();
-        issue_ids(1);
-        issue_rows(0);
-    }
-
-    for (int kt = 0;; kt++) {
-        int t, nrow;
-        int64_t i0;
-        if (!tile_info(kt, t, i0, nrow)) break;
-        const ds_table_desc &td = a.t[t];
-        const int64_t ids_base = s_sched[2 * nt + 1 + t];
-        const int64_t *tile_ids = ids_sh + (size_t)(kt % 3) * TR;
-        const float *tile_rows = rows_sh + (size_t)(kt & 1) * TR * d;
-
-        if (MODE != 2) {
-            cp_async_wait<1>();  // ids(kt+1) landed (rows(kt) may still be in flight)
-            __syncthreads();
-            issue_ids(kt + 2);
-            issue_rows(kt + 1);
-            cp_async_wait<2>();  // rows(kt) landed: own copies only, no CTA barrier
-        }
-
-        for (int p = 0; p < TR; p += RPP) {
-            const int r = p + slot;
-            bool valid = r < nrow;
-            if (!__any_sync(DS_FULL_MASK, valid)) continue;
-            int64_t local = 0;
-            float x[EPL];
-            if (MODE != 2) {
-                if (valid) {
-                    local = a.incremental ? local_of(td, tile_ids[r]) : i0 + r;
-                    if (local < 0) {
-                        bad_ids = true;
-                        valid = false;
-                        local = 0;
-                    }
-                }
-                if (valid) {
-                    const float *row = tile_rows + r * d;
-                    if (VEC == 4) {
-#pragma unroll
-                        for (int c = 0; c < C; c++) {
-                            int e = 4 * (lig + c * G);
-                            float4 v = e < d ? *reinterpret_cast<const float4 *>(row + e)
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
-                            x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < C; k++) {
-                            int e = lig + k * G;
-                            x[k] = e < d ? row[e] : 0.f;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < EPL; k++) x[k] = 0.f;
-                }
-            } else {
-                if (valid) {
-                    const int64_t i = i0 + r;
-                    local = i;
-                    if (a.incremental) {
-                        int64_t id = __ldg(a.ids + ids_base + i);
-                        local = a.ids_local ? id : id - td.row_base;
-                        if (local < 0 || local >= td.rows) {
-                            bad_ids = true;
-                            valid = false;
-                            local = 0;
-                        }
-                    }
-                }
-                if (valid) load_row<G, C, VEC>(td.values + local * td.ld, d, lig, x, 0.f);
-                else
-#pragma unroll
-                    for (int k = 0; k < EPL; k++) x[k] = 0.f;
-            }
-            const int64_t gid = td.row_base + local;
-            uint8_t *rec = stage + r * a.rec;
-            if (valid && a.incremental && lig == 0) {
-                if ((reinterpret_cast<uintptr_t>(rec) & 7) == 0)
-                    *reinterpret_cast<uint64_t *>(rec) = (uint64_t)gid;
-                else
-                    st_bytes(rec, (uint64_t)gid, 8);
-            }
-
-            if (MODE == 0) {
-                if (valid) {
-#pragma unroll
-                    for (int k = 0; k < EPL; k++) {
-                        int e = Lay::elem(lig, k);
-                        if (e < d) st_u32(rec + a.par_off + 4 * e, __float_as_uint(x[k]));
-                    }
-                }
-            } else {
-                // finiteness (quant.py:70-72,173): x*0 is NaN exactly for NaN/Inf;
-                // naive range: row min / max (engine.py:163-164)
-                float nz = 0.f, mn = INFINITY, mx = -INFINITY;
-#pragma unroll
-                for (int k = 0; k < EPL; k++) {
-                    if (!PAD || Lay::elem(lig, k) < d) {
-                        nz = __fmaf_rn(x[k], 0.f, nz);
-                        mn = fminf(mn, x[k]);
-                        mx = fmaxf(mx, x[k]);
-                    }
-                }
-                const bool fin = grp_sum<G>(nz) == 0.f;
-                if (valid && !fin) bad_data = true;
-                const bool row_ok = valid && fin;
-                float lo = grp_min<G>(mn), hi = grp_max<G>(mx);
-                if (!row_ok) { lo = 0.f; hi = 0.f; }
-                if (MODE == 2) {
-                    double *buf = exact_sh + slot * (d + 8);
-                    greedy_row<G, C, VEC, PAD>(x, d, lig, row_ok, lo, hi, L, a.bins, a.steps, buf,
-                                               lo, hi, n_exact_dec, n_exact_codes);
-                }
-                const RowQ rq = make_rowq(lo, hi, L, a.invL);
-                float qf[EPL];
-                if (MODE == 1) {
-                    // min/max ranges hold every element: no clip, v in [0, L(1+5u)];
-                    // one deviation test per row replaces per-element branches
-                    float dev = 0.f;
-#pragma unroll
-                    for (int k = 0; k < EPL; k++) {
-                        float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
-                        qf[k] = rintf(v);
-                        dev = fmaxf(dev, fabsf(__fsub_rn(v, qf[k])));
-                    }
-                    dev = grp_max<G>(dev);
-                    if (row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps)) {
-                        // rare: a code within the guard band of a tie -> exact f64
-#pragma unroll
-                        for (int k = 0; k < EPL; k++) {
-                            if (!PAD || Lay::elem(lig, k) < d) {
-                                qf[k] = (float)code_exact_slow(x[k], lo, hi, rq.s, L);
-                                n_exact_codes++;
-                            }
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < EPL; k++) qf[k] = (float)code_of(x[k], rq, n_exact_codes);
-                }
-                int q[EPL];
-                double sse = 0.0;
-#pragma unroll
-                for (int k = 0; k < EPL; k++) {
-                    const bool in = row_ok && (!PAD || Lay::elem(lig, k) < d);
-                    if (!in) qf[k] = 0.f;
-                    // code as an integer from the float bits (q < 2^22): 1.5*2^23 + q
-                    q[k] = __float_as_int(__fadd_rn(qf[k], 12582912.0f)) & 0x3fffff;
-                    // err_sum term (engine.py:171-173): exact dequantized value
-                    float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf[k]), (double)lo));
-                    double er = __dsub_rn((double)x[k], (double)dq);
-                    sse = in ? fma(er, er, sse) : sse;
-                }
-                sse = grp_sumd<G>(sse);
-                if (row_ok && lig == 0) {
-                    err_acc += sqrt(sse);
-                    n_rows++;
-                    st_u32(rec + a.par_off, __float_as_uint(lo));
-                    st_u32(rec + a.par_off + 4, __float_as_uint(hi));
-                }
-                // ---- pack (quant.py:376-382): LSB-first bitstream ----
-                uint8_t *pk = rec + a.code_off;
-                if (VEC == 4 && (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2)) {
-                    if (valid) {
-#pragma unroll
-                        for (int c = 0; c < C; c++) {
-                            int m = lig + c * G;  // chunk index: elements 4m..4m+3
-                            if (4 * m < d) {
-                                uint32_t v;
-                                if (a.bitwidth == 8) {
-                                    v = q[4 * c] | (q[4 * c + 1] << 8) | (q[4 * c + 2] << 16) |
-                                        ((uint32_t)q[4 * c + 3] << 24);
-                                    st_u32(pk + 4 * m, v);
-                                } else if (a.bitwidth == 4) {
-                                    v = q[4 * c] | (q[4 * c + 1] << 4) | (q[4 * c + 2] << 8) |
-                                        (q[4 * c + 3] << 12);
-                                    st_bytes(pk + 2 * m, v, 2);
-                                } else {
-                                    v = q[4 * c] | (q[4 * c + 1] << 2) | (q[4 * c + 2] << 4) |
-                                        (q[4 * c + 3] << 6);
-                                    pk[m] = (uint8_t)v;
-                                }
-                            }
-                        }
-                    }
-                } else {
-                    // generic: codes through shared memory, each lane builds bytes
-                    uint8_t *cs = codes_sh + slot * d;
-                    if (valid) {
-#pragma unroll
-                        for (int k = 0; k < EPL; k++) {
-                            int e = Lay::elem(lig, k);
-                            if (e < d) cs[e] = (uint8_t)q[k];
-                        }
-                    }
-                    __syncwarp();
-                    if (valid) {
-                        const int N = a.bitwidth;
-                        for (int b = lig; b < a.packed; b += G) {
-                            int bit0 = 8 * b;
-                            int j0 = bit0 / N, j1 = min(d - 1, (bit0 + 7) / N);
-                            uint32_t v = 0;
-                            for (int j = j0; j <= j1; j++) {
-                                int pos = j * N - bit0;
-                                uint32_t cv = cs[j];
-                                v |= pos >= 0 ? (cv << pos) : (cv >> (-pos));
-                            }
-                            pk[b] = (uint8_t)v;
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-            if (a.aux && valid) {
-                float xa[EPL];
-                load_row<G, C, VEC>(td.aux + local * td.ld, d, lig, xa, 0.f);
+        } else {
+            // generic: codes through shared memory, each lane builds bytes
+            if (valid) {
 #pragma unroll
                 for (int k = 0; k < EPL; k++) {
                     int e = Lay::elem(lig, k);
-                    if (e < d) st_u32(rec + a.aux_off + 4 * e, __float_as_uint(xa[k]));
+                    if (e < d) cs[e] = (uint8_t)q[k];
                 }
             }
+            __syncwarp();
+            if (valid) {
+                const int N = a.bitwidth;
+                for (int b = lig; b < a.packed; b += G) {
+                    int bit0 = 8 * b;
+                    int j0 = bit0 / N, j1 = min(d - 1, (bit0 + 7) / N);
+                    uint32_t v = 0;
+                    for (int j = j0; j <= j1; j++) {
+                        int pos = j * N - bit0;
+                        uint32_t cv = cs[j];
+                        v |= pos >= 0 ? (cv << pos) : (cv >> (-pos));
+                    }
+                    pk[b] = (uint8_t)v;
+                }
+            }
+            __syncwarp();
         }
-        __syncthreads();
-        int64_t dst = a.sec_off[t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
-        copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec);
-        __syncthreads();
     }
-    if (MODE != 2) cp_async_wait<0>();  // nothing may land after the CTA exits
+    if (a.aux && valid) {
+        float xa[EPL];
+        load_row<G, C, VEC>(td.aux + local * td.ld, d, lig, xa, 0.f);
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            int e = Lay::elem(lig, k);
+            if (e < d) st_u32(rec + a.aux_off + 4 * e, __float_as_uint(xa[k]));
+        }
+    }
+    return fix;
+}
 
-    // per-CTA error partial (deterministic final sum in err_reduce_kernel)
-    for (int o = 16; o > 0; o >>= 1) err_acc += __shfl_xor_sync(DS_FULL_MASK, err_acc, o);
-    if (lane == 0) s_red[threadIdx.x >> 5] = err_acc;
-    if (__any_sync(DS_FULL_MASK, bad_data) && lane == 0) atomicOr(a.flags, DS_FLAG_DATA);
-    if (__any_sync(DS_FULL_MASK, bad_ids) && lane == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
+// block-level epilogue: error partial (deterministic final sum in
+// err_reduce_kernel), flags, diagnostics
+__device__ __forceinline__ void writer_epilogue(const WriterArgs &a, WAcc &acc, double *s_red) {
+    const int lane = threadIdx.x & 31;
+    for (int o = 16; o > 0; o >>= 1) acc.err += __shfl_xor_sync(DS_FULL_MASK, acc.err, o);
+    if (lane == 0) s_red[threadIdx.x >> 5] = acc.err;
+    if (__any_sync(DS_FULL_MASK, acc.bad_data) && lane == 0) atomicOr(a.flags, DS_FLAG_DATA);
+    if (__any_sync(DS_FULL_MASK, acc.bad_ids) && lane == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
     if (a.stats) {
-        unsigned v0 = n_exact_dec, v1 = n_exact_codes, v2 = n_rows;
+        unsigned v0 = acc.n_exact_dec, v1 = acc.n_exact_codes, v2 = acc.n_rows;
         for (int o = 16; o > 0; o >>= 1) {
             v0 += __shfl_xor_sync(DS_FULL_MASK, v0, o);
             v1 += __shfl_xor_sync(DS_FULL_MASK, v1, o);
@@ -494,6 +339,351 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? 1 : 4) writer_kernel(const Wri
         for (int w = 0; w < WT / 32; w++) s += s_red[w];
         a.partials[blockIdx.x] = s;
     }
+}
+
+// table of a tile: the last table whose first tile is <= tile (one ballot
+// per 32 tables; warp-uniform)
+__device__ __forceinline__ int tile_table(const int64_t *s_sched, int nt, int64_t tile, int lane) {
+    int t = 0;
+    for (int b = 0; b < nt; b += 32) {
+        unsigned m = __ballot_sync(DS_FULL_MASK, b + lane < nt && s_sched[b + lane] <= tile);
+        if (m) t = b + 31 - __clz(m);
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// MODE 1 fixup: re-code, in exact f64, the rows of one warp-tile that the
+// hot loop flagged (a code within the fp32 guard band of a tie, or a range
+// outside fp32's comfort zone; ~0.3% of rows on realistic data).  Called by
+// each warp after its tile loop for its own flagged tiles, so the f64 code
+// shares no live range with the hot loop and the error sum stays in a fixed
+// order.  The packed codes of each flagged record are overwritten in the
+// payload; the rows' exact errors are added (the hot loop left them out).
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC, bool PAD>
+__device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_sched, int64_t tile,
+                                         unsigned m, uint8_t *cs_warp, int d, WAcc &acc) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int lig = lane & (G - 1), slot = lane / G;
+    const int nt = a.ntables;
+    const int t = tile_table(s_sched, nt, tile, lane);
+    const ds_table_desc &td = a.t[t];
+    const int64_t i0 = (tile - s_sched[t]) * RPW;
+    const bool mine = (m >> (slot * G)) & 1u;
+    uint8_t *cs = cs_warp + slot * d;
+    int64_t local = 0;
+    if (mine) {
+        local = i0 + slot;
+        if (a.incremental) {
+            const int64_t raw = a.ids[s_sched[2 * nt + 1 + t] + i0 + slot];
+            local = a.ids_local ? raw : raw - td.row_base;  // validated by the hot loop
+        }
+    }
+    float x[EPL];
+    if (mine) load_row<G, C, VEC>(td.values + local * td.ld, d, lig, x, 0.f);
+    else
+#pragma unroll
+        for (int k = 0; k < EPL; k++) x[k] = 0.f;
+    float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < EPL; k++)
+        if (!PAD || Lay::elem(lig, k) < d) {
+            mn = fminf(mn, x[k]);
+            mx = fmaxf(mx, x[k]);
+        }
+    const float lo = grp_min<G>(mn), hi = grp_max<G>(mx);
+    const RowQ rq = make_rowq(lo, hi, a.L, a.invL);
+    // the hot loop's codes, exact codes for the ambiguous elements only
+    int qfast[EPL], qex[EPL];
+    bool changed = false;
+#pragma unroll
+    for (int k = 0; k < EPL; k++) {
+        const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
+        const float qm = __fadd_rn(v, 12582912.0f);
+        qfast[k] = __float_as_int(qm) & 0x3fffff;
+        qex[k] = qfast[k];
+        const bool in = mine && (!PAD || Lay::elem(lig, k) < d);
+        if (in && (rq.mode == 2 || fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))) > 0.5f - rq.eps)) {
+            qex[k] = code_exact(x[k], lo, hi, rq.s, a.L);
+            acc.n_exact_codes++;
+            changed |= qex[k] != qfast[k];
+        }
+    }
+    // a fast code was wrong (exact ties; rare): replace the record's codes and
+    // swap the row's error contribution
+    // (range outside fp32's comfort zone: the hot loop left the error out)
+    const int any_changed = grp_or<G>(changed ? 1 : 0);  // every lane shuffles
+    const bool row_changed = mine && (rq.mode == 2 || any_changed != 0);
+    if (__any_sync(DS_FULL_MASK, row_changed)) {
+        double sf = 0.0, se = 0.0;
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            const int e = Lay::elem(lig, k);
+            if (row_changed && e < d) {
+                const double ef = __dsub_rn((double)x[k], (double)deq_exact(qfast[k], lo, rq.s));
+                const double ee = __dsub_rn((double)x[k], (double)deq_exact(qex[k], lo, rq.s));
+                sf = fma(ef, ef, sf);
+                se = fma(ee, ee, se);
+                cs[e] = (uint8_t)qex[k];
+            }
+        }
+        sf = grp_sumd<G>(sf);
+        se = grp_sumd<G>(se);
+        if (row_changed && lig == 0)
+            acc.err += (se > 0.0 ? se * rsqrt(se) : 0.0) -
+                       (rq.mode == 2 || !(sf > 0.0) ? 0.0 : sf * rsqrt(sf));
+        __syncwarp();
+        if (row_changed) {  // overwrite the record's packed codes (LSB-first bitstream)
+            uint8_t *pk = a.payload + a.sec_off[t] + (a.write_headers ? DS_HEADER_SIZE : 0) +
+                          (i0 + slot) * a.rec + a.code_off;
+            const int N = a.bitwidth;
+            for (int b = lig; b < a.packed; b += G) {
+                const int bit0 = 8 * b;
+                const int j0 = bit0 / N, j1 = min(d - 1, (bit0 + 7) / N);
+                uint32_t v = 0;
+                for (int j = j0; j <= j1; j++) {
+                    const int pos = j * N - bit0;
+                    const uint32_t cv = cs[j];
+                    v |= pos >= 0 ? (cv << pos) : (cv >> (-pos));
+                }
+                pk[b] = (uint8_t)v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// MODE 0/1: HBM-bound gather.  Every warp runs its own pipeline over
+// warp-tiles of 32/G consecutive records (no CTA barriers): the ids of tile
+// k+2 and the rows of tile k+1 are in flight (cp.async groups into the warp's
+// shared memory) while tile k is coded into the warp's record stage, which
+// then streams to HBM as one contiguous run.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int align16(int v) { return (v + 15) & ~15; }
+
+template <int G, int C, int VEC, int MODE, bool PAD>
+__global__ void __launch_bounds__(WT, 3) writer_warp_kernel(const WriterArgs a) {
+    constexpr int EPL = C * VEC;
+    constexpr int RPW = 32 / G;  // records per warp-tile
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int d = PAD ? a.dim : (VEC == 4 ? 4 * G * C : G * C);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lig = lane & (G - 1);
+    const int slot = lane / G;  // record of the warp-tile this group codes
+    // per-warp shared memory (host computes the same sizes)
+    const int stage_b = align16(RPW * a.rec) + 16;
+    const int codes_b = align16(RPW * d);
+    const int rows_b = align16(RPW * d * 4);
+    const int warp_b = stage_b + codes_b + 2 * rows_b + 3 * RPW * 8;
+    // 16-byte aligned carve-up whatever the static shared memory in front
+    uint8_t *smem_al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 15) & ~(uintptr_t)15);
+    uint8_t *wbase = smem_al + (size_t)wid * warp_b;
+    uint8_t *stage = wbase;
+    uint8_t *codes = wbase + stage_b;
+    float *rows_sh = reinterpret_cast<float *>(codes + codes_b);
+    int64_t *ids_sh = reinterpret_cast<int64_t *>(codes + codes_b + 2 * rows_b);
+
+    __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
+    __shared__ double s_red[WT / 32];
+    const int nt = a.ntables;
+    for (int k = threadIdx.x; k < 3 * nt + 1; k += WT) s_sched[k] = a.sched[k];
+    __syncthreads();
+    WAcc acc;
+    if (a.sec_off[nt] <= a.capacity) {  // else flagged by the layout kernel
+        const int64_t total_tiles = s_sched[nt];
+        const int64_t gw = (int64_t)blockIdx.x * (WT / 32) + wid;
+        const int64_t nwarps = (int64_t)gridDim.x * (WT / 32);
+        // tile k of this warp -> (table, first record, records); each tile is
+        // looked up once and carried through a 3-deep ring (ids k+2, rows k+1,
+        // coding k)
+        struct TI {
+            int t, nrow;
+            int64_t i0;
+            bool ok;
+        };
+        auto info = [&](int k) -> TI {
+            TI r;
+            const int64_t tile = gw + (int64_t)k * nwarps;
+            r.ok = tile < total_tiles;
+            r.t = r.ok ? tile_table(s_sched, nt, tile, lane) : 0;
+            r.i0 = r.ok ? (tile - s_sched[r.t]) * RPW : 0;
+            r.nrow = r.ok ? (int)min((int64_t)RPW, s_sched[nt + 1 + r.t] - r.i0) : 0;
+            return r;
+        };
+        auto local_of = [&](const ds_table_desc &td, int64_t raw) -> int64_t {
+            // ids from capture are table-local; plan ids are global
+            int64_t local = a.ids_local ? raw : raw - td.row_base;
+            return (local < 0 || local >= td.rows) ? -1 : local;
+        };
+        auto issue_ids = [&](const TI &ti, int k) {
+            if (a.incremental && ti.ok && lane < ti.nrow)
+                cp_async8(ids_sh + (k % 3) * RPW + lane,
+                          a.ids + s_sched[2 * nt + 1 + ti.t] + ti.i0 + lane);
+            cp_async_commit();
+        };
+        auto issue_rows = [&](const TI &ti, int k) {
+            if (ti.ok && slot < ti.nrow) {
+                const ds_table_desc &td = a.t[ti.t];
+                const int64_t local = a.incremental ? local_of(td, ids_sh[(k % 3) * RPW + slot])
+                                                    : ti.i0 + slot;
+                if (local >= 0) {
+                    const float *src = td.values + local * td.ld;
+                    float *dst = rows_sh + (k & 1) * (rows_b / 4) + slot * d;
+#pragma unroll
+                    for (int c = 0; c < C; c++) {
+                        if (VEC == 4) {
+                            int e = 4 * (lig + c * G);
+                            if (e < d) cp_async16(dst + e, src + e);
+                        } else {
+                            int e = lig + c * G;
+                            if (e < d) cp_async4(dst + e, src + e);
+                        }
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+        // prologue: ids(0) landed; ids(1) and rows(0) in flight
+        TI cur = info(0), nxt = info(1);
+        issue_ids(cur, 0);
+        cp_async_wait<0>();
+        __syncwarp();
+        issue_ids(nxt, 1);
+        issue_rows(cur, 0);
+        for (int k = 0; cur.ok; k++) {
+            const TI far = info(k + 2);
+            const ds_table_desc &td = a.t[cur.t];
+            cp_async_wait<1>();  // ids(k+1) landed (rows(k) may still be in flight)
+            __syncwarp();
+            issue_ids(far, k + 2);
+            issue_rows(nxt, k + 1);
+            cp_async_wait<2>();  // rows(k) landed: each lane reads only its own copies
+            const int nrow = cur.nrow;
+            const int64_t i0 = cur.i0;
+            bool valid = slot < nrow;
+            int64_t local = 0;
+            if (valid) {
+                local = a.incremental ? local_of(td, ids_sh[(k % 3) * RPW + slot]) : i0 + slot;
+                if (local < 0) {
+                    acc.bad_ids = true;
+                    valid = false;
+                    local = 0;
+                }
+            }
+            float x[EPL];
+            const float *row = rows_sh + (k & 1) * (rows_b / 4) + slot * d;
+            if (VEC == 4) {
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    int e = 4 * (lig + c * G);
+                    float4 v = (valid && e < d) ? *reinterpret_cast<const float4 *>(row + e)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < C; kk++) {
+                    int e = lig + kk * G;
+                    x[kk] = (valid && e < d) ? row[e] : 0.f;
+                }
+            }
+            const bool fix = code_row<G, C, VEC, MODE, PAD>(a, td, x, row, valid, local,
+                                                            stage + slot * a.rec, codes + slot * d,
+                                                            nullptr, lig, d, acc);
+            // rows for the fixup pass below: one bit per group leader lane
+            const unsigned fixm = __ballot_sync(DS_FULL_MASK, fix && lig == 0);
+            if (MODE == 1 && lane == 0) a.fix_mask[gw + (int64_t)k * nwarps] = fixm;
+            __syncwarp();
+            const int64_t dst = a.sec_off[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
+            copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec, lane, 32);
+            __syncwarp();  // the stage is rewritten by the next tile
+            cur = nxt;
+            nxt = far;
+        }
+        cp_async_wait<0>();  // nothing may land after the warp exits
+        if (MODE == 1) {
+            // exact re-coding of this warp's flagged rows (its tiles, in order)
+            __syncwarp();
+            for (int64_t tile = gw; tile < total_tiles; tile += nwarps) {
+                const unsigned m = a.fix_mask[tile];
+                if (m) fix_tile<G, C, VEC, PAD>(a, s_sched, tile, m, codes, d, acc);
+            }
+        }
+    }
+    writer_epilogue(a, acc, s_red);
+}
+
+// ---------------------------------------------------------------------------
+// MODE 2 (greedy ranges): compute-bound (~20 candidate evaluations per row);
+// rows load straight into registers, one pass of WT/G rows per tile.
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC, int MODE, bool PAD>
+__global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
+    constexpr int EPL = C * VEC;
+    constexpr int RPP = WT / G;  // rows per pass
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int TR = a.tile_rows;
+    const int d = PAD ? a.dim : (VEC == 4 ? 4 * G * C : G * C);
+    const int stage_bytes = align16(TR * a.rec) + 16;
+    uint8_t *stage = smem;
+    uint8_t *codes_sh = smem + stage_bytes;                                 // RPP * d bytes
+    double *exact_sh = reinterpret_cast<double *>(codes_sh + align16(RPP * d));  // RPP*(d+8)
+
+    __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
+    __shared__ double s_red[WT / 32];
+    const int nt = a.ntables;
+    for (int k = threadIdx.x; k < 3 * nt + 1; k += WT) s_sched[k] = a.sched[k];
+    __syncthreads();
+    WAcc acc;
+    const int lane = threadIdx.x & 31;
+    const int lig = lane & (G - 1);
+    const int slot = threadIdx.x / G;
+    if (a.sec_off[nt] <= a.capacity) {  // else flagged by the layout kernel
+        const int64_t total_tiles = s_sched[nt];
+        for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            const int t = tile_table(s_sched, nt, tile, lane);
+            const ds_table_desc &td = a.t[t];
+            const int64_t i0 = (tile - s_sched[t]) * TR;
+            const int nrow = (int)min((int64_t)TR, s_sched[nt + 1 + t] - i0);
+            const int64_t ids_base = s_sched[2 * nt + 1 + t];
+            for (int p = 0; p < TR; p += RPP) {
+                const int r = p + slot;
+                bool valid = r < nrow;
+                if (!__any_sync(DS_FULL_MASK, valid)) continue;
+                int64_t local = 0;
+                if (valid) {
+                    local = i0 + r;
+                    if (a.incremental) {
+                        int64_t id = __ldg(a.ids + ids_base + i0 + r);
+                        local = a.ids_local ? id : id - td.row_base;
+                        if (local < 0 || local >= td.rows) {
+                            acc.bad_ids = true;
+                            valid = false;
+                            local = 0;
+                        }
+                    }
+                }
+                float x[EPL];
+                if (valid) load_row<G, C, VEC>(td.values + local * td.ld, d, lig, x, 0.f);
+                else
+#pragma unroll
+                    for (int k = 0; k < EPL; k++) x[k] = 0.f;
+                code_row<G, C, VEC, MODE, PAD>(a, td, x, nullptr, valid, local, stage + r * a.rec,
+                                               codes_sh + slot * d, exact_sh + slot * (d + 8), lig,
+                                               d, acc);
+            }
+            __syncthreads();
+            const int64_t dst = a.sec_off[t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
+            copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec, threadIdx.x, WT);
+            __syncthreads();
+        }
+    }
+    writer_epilogue(a, acc, s_red);
 }
 
 // ---------------------------------------------------------------------------
@@ -534,7 +724,11 @@ static Cfg pick_cfg(int d, bool vec4) {
 template <int MODE, bool PAD>
 static writer_fn select_writer(const Cfg &c) {
 #define DS_W(G_, C_, V_) \
-    if (c.G == G_ && c.C == C_ && c.VEC == V_) return writer_kernel<G_, C_, V_, MODE, PAD>;
+    if (c.G == G_ && c.C == C_ && c.VEC == V_)                                                  \
+    {                                                                                            \
+        if constexpr (MODE == 2) return writer_kernel<G_, C_, V_, MODE, PAD>;                    \
+        else return writer_warp_kernel<G_, C_, V_, MODE, PAD>;                                   \
+    }
     DS_W(1, 1, 4) DS_W(1, 2, 4) DS_W(1, 4, 4) DS_W(2, 4, 4) DS_W(4, 4, 4) DS_W(8, 4, 4)
     DS_W(16, 4, 4) DS_W(32, 4, 4) DS_W(32, 8, 4)
     DS_W(1, 1, 1) DS_W(1, 2, 1) DS_W(1, 4, 1) DS_W(1, 8, 1) DS_W(1, 16, 1) DS_W(2, 16, 1)

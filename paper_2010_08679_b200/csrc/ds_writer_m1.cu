@@ -6,4 +6,5 @@ namespace ds {
 writer_fn select_writer_mode1(const Cfg &c, bool pad) {
     return pad ? select_writer<1, true>(c) : select_writer<1, false>(c);
 }
+
 }  // namespace ds

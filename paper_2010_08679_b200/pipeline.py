@@ -1,0 +1,94 @@
+"""Overlapped host <-> device checkpoint pipeline for one rank.
+
+The stall-window work of a checkpoint (K1 mark, K2 capture, K3 write) runs on
+the compute stream; the next interval's lookups stream in (H2D) and the
+previous checkpoint's payload streams out (D2H) on copy streams, so PCIe
+transfers overlap the kernels (the paper's "background" write, engine.py:
+347-411, with the quantization moved onto the GPU).
+
+    pipe = CheckpointPipeline(checkpointer, idx_capacity)
+    for host_idx in interval_lookups:          # pinned host tensors
+        pipe.submit(host_idx, seg_off, seg_tables)
+    payloads = pipe.drain()                    # [(bytes view, nbytes), ...]
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .sharded import ShardedCheckpointer
+
+
+class CheckpointPipeline:
+    """Double-buffered H2D -> compute -> D2H pipeline over a ShardedCheckpointer."""
+
+    def __init__(self, ck: ShardedCheckpointer, idx_capacity: int, idx_dtype=torch.int32,
+                 keep_outputs: bool = False):
+        self.ck = ck
+        dev = ck.device
+        self.compute = torch.cuda.current_stream(dev)
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.idx = [torch.empty(idx_capacity, dtype=idx_dtype, device=dev) for _ in range(2)]
+        self.payload = [ck.payload, torch.empty_like(ck.payload)]
+        self.host_out = [torch.empty(ck.payload.numel(), dtype=torch.uint8, pin_memory=True)
+                         for _ in range(2)]
+        self.nbytes_host = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+        self.flags_host = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_done = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.k = 0
+        self.pending = None  # (slot) whose D2H is not issued yet
+        self.keep = keep_outputs
+        self.outputs = []
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _issue_d2h(self, slot: int) -> None:
+        self.ev_done[slot].synchronize()        # its counts are on the host now
+        _lib.raise_flags(int(self.flags_host[slot]), "checkpoint")
+        n = int(self.nbytes_host[slot])
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.ev_done[slot])
+            self.host_out[slot][:n].copy_(self.payload[slot][:n], non_blocking=True)
+            self.ev_out[slot].record(self.d2h)
+        self.d2h_bytes += n
+        if self.keep:
+            self.outputs.append((slot, n))
+
+    def submit(self, host_idx: torch.Tensor, seg_off, seg_tables) -> None:
+        """Queue one checkpoint interval whose lookups are in pinned host memory."""
+        s = self.k & 1
+        n = host_idx.numel()
+        # H2D: the slot's index buffer was last read by step k-2
+        with torch.cuda.stream(self.h2d):
+            if self.k >= 2:
+                self.h2d.wait_event(self.ev_done[s])
+            self.idx[s][:n].copy_(host_idx, non_blocking=True)
+            self.ev_in[s].record(self.h2d)
+        self.h2d_bytes += n * host_idx.element_size()
+        # compute: the slot's payload buffer must have left (D2H of step k-2)
+        self.compute.wait_event(self.ev_in[s])
+        if self.k >= 2:
+            self.compute.wait_event(self.ev_out[s])
+        self.ck.payload = self.payload[s]
+        self.ck.step(self.idx[s][:n], seg_off, seg_tables)
+        self.nbytes_host[s:s + 1].copy_(self.ck.writer.sec_off[-1:], non_blocking=True)
+        self.flags_host[s:s + 1].copy_(self.ck.writer.flags, non_blocking=True)
+        self.ev_done[s].record(self.compute)
+        # D2H of the previous step overlaps this step's kernels
+        if self.pending is not None:
+            self._issue_d2h(self.pending)
+        self.pending = s
+        self.k += 1
+
+    def drain(self):
+        """Issue the last D2H and wait for every transfer."""
+        if self.pending is not None:
+            self._issue_d2h(self.pending)
+            self.pending = None
+        self.d2h.synchronize()
+        self.compute.synchronize()
+        return [(self.host_out[s], n) for s, n in self.outputs]

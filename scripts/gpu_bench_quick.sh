@@ -1,8 +1,8 @@
 #!/bin/bash
 # quick GPU check: gpu tests + one bench line (+ optional ncu of the named kernels)
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python bench.py --no-cpu > gpurun_out/bq.json 2> gpurun_out/bq.err; echo "bench rc=$?"
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python bench.py --no-cpu > gpurun_out/bq.json 2> gpurun_out/bq.err; echo "bench rc=$?"
 python - <<'P'
 import json
 d=json.load(open("gpurun_out/bq.json"))
@@ -12,7 +12,7 @@ print(" roofline", d["roofline"]["kernel"], round(d["roofline"]["frac"],3), "clo
 P
 if [ -n "${NCU_K:-}" ]; then
   CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
-  $CMD > gpurun_out/plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"$NCU_K" -s ${NCU_S:-4} -c ${NCU_C:-3} \
+  timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$NCU_K" -s ${NCU_S:-4} -c ${NCU_C:-3} \
       -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?"
 fi

@@ -311,6 +311,50 @@ def test_payload_dims_vs_oracle(ds, O, d, bw):
         assert err == pytest.approx(err_ref, rel=1e-12, abs=1e-300)
 
 
+@pytest.mark.parametrize("bw", (2, 3, 4, 8))
+@pytest.mark.parametrize("d", (16, 20, 128))
+def test_writer_tie_heavy_rows_vs_oracle(ds, O, bw, d):
+    """Grid-valued rows put many codes exactly on ties: every one of them goes
+    through the exact-f64 fixup pass and must still match bit for bit."""
+    rng = np.random.default_rng(bw * 100 + d)
+    rows = 4000
+    grid = rng.integers(-64, 64, (rows, d)).astype(np.float32) / np.float32(8)
+    grid[::3] = (np.arange(d) % 7).astype(np.float32) * np.float32(0.5)  # exact half-steps
+    grid[1::5] *= np.float32(1e-3)
+    tabs = {0: _Tab(0, grid)}
+    sel = {0: np.arange(0, rows, 2, dtype=np.int64)}
+    for kind in ("incremental", "full"):
+        plan = _Plan(kind, sel if kind == "incremental" else None, bw)
+        ov = {bw: ds.AdaptiveConfig(1, 0.5)}  # naive ranges also at 2/3/4 bits
+        blob, qr, err = ds.build_shard_payload(_Snap(tabs, 1), plan, 0, 1024, ov)
+        ref, qr_ref, err_ref = O.build_shard_payload({0: (grid, None)}, kind, sel, bw, [0],
+                                                     adaptive={bw: (1, 0.5)}, nthreads=8)
+        assert blob == ref
+        assert err == pytest.approx(err_ref, rel=1e-12, abs=1e-300)
+
+
+@pytest.mark.parametrize("bw", (2, 8))
+def test_writer_extreme_range_rows_vs_oracle(ds, O, bw):
+    """Rows whose range leaves fp32's comfort zone (huge, tiny, subnormal)
+    take the exact path for every code and for their error term."""
+    rng = np.random.default_rng(7 + bw)
+    rows, d = 600, 16
+    x = rng.standard_normal((rows, d)).astype(np.float32)
+    x[0::6] *= np.float32(1e37)
+    x[1::6, :8] = np.float32(-3.0e38)
+    x[1::6, 8:] = np.float32(3.0e38)
+    x[2::6] = np.float32(1.0) + x[2::6] * np.float32(1e-33)
+    x[3::6] *= np.float32(1e-40)  # subnormal
+    x[4::6] = np.float32(5.0)  # constant rows
+    tabs = {0: _Tab(0, x)}
+    blob, qr, err = ds.build_shard_payload(_Snap(tabs, 1), _Plan("full", None, bw), 0, 1024,
+                                           {bw: ds.AdaptiveConfig(1, 0.5)})
+    ref, qr_ref, err_ref = O.build_shard_payload({0: (x, None)}, "full", None, bw, [0],
+                                                 adaptive={bw: (1, 0.5)}, nthreads=8)
+    assert blob == ref
+    assert err == pytest.approx(err_ref, rel=1e-12)
+
+
 def test_writer_errors(ds):
     x = np.zeros((10, 4), np.float32)
     x[3, 1] = np.nan
