@@ -168,7 +168,11 @@ typedef struct {
  * counts[t]; full checkpoints pass NULL and use rows), computes on device
  *   sec_off[t]   byte offset of table t's section (header) in the payload,
  *   sec_off[ntables] total payload bytes,
- * and the tile schedule the writer uses.  Everything stays on device. */
+ * and the tile schedule the writer uses.  Everything stays on device; the
+ * whole call is ONE kernel launch (layout, records, exact fixups, error sum).
+ * The workspace must be zero-filled before its first use and not be shared
+ * by calls in flight at the same time (it holds a completion counter that
+ * each call leaves at zero). */
 DS_API size_t ds_writer_workspace_size(int ntables, int64_t max_rows, int64_t dim);
 DS_API int ds_write_payload(const ds_table_desc *tables_host, int ntables, const ds_ckpt_params *p,
                      const int64_t *ids, const int64_t *counts, uint8_t *payload,

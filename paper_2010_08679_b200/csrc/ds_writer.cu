@@ -1,58 +1,10 @@
-// ds_writer.cu -- K3 host side: layout kernel, error reduction, C ABI entry.
+// ds_writer.cu -- K3 host side: launch configuration and the C ABI entry.
 //
 // The writer kernel itself is ds_writer.cuh (instantiated per mode in
 // ds_writer_m0.cu / ds_writer_m1.cu / ds_writer_m2.cu).
 #include "ds_writer.cuh"
 
 namespace ds {
-
-// ---------------------------------------------------------------------------
-// layout: section offsets, headers (payload.py:88-91), tile schedule
-// ---------------------------------------------------------------------------
-__global__ void layout_kernel(const WriterArgs a) {
-    if (threadIdx.x != 0) return;
-    int64_t off = 0, tiles = 0, ids = 0;
-    int nt = a.ntables;
-    for (int t = 0; t < nt; t++) {
-        int64_t n = a.counts ? a.counts[t] : a.t[t].rows;
-        a.sched[t] = tiles;
-        a.sched[nt + 1 + t] = n;
-        a.sched[2 * nt + 1 + t] = a.ids_packed ? ids : a.t[t].ids_off;
-        ids += n;
-        a.sec_off[t] = off;
-        if (a.write_headers) {
-            if (off + DS_HEADER_SIZE <= a.capacity) {
-                uint8_t *h = a.payload + off;
-                h[0] = 'C'; h[1] = 'N'; h[2] = 'R'; h[3] = '1';
-                uint32_t tid = a.t[t].table_id, dim = a.t[t].dim;
-                for (int k = 0; k < 4; k++) h[4 + k] = (uint8_t)(tid >> (8 * k));
-                for (int k = 0; k < 8; k++) h[8 + k] = (uint8_t)((uint64_t)n >> (8 * k));
-                for (int k = 0; k < 4; k++) h[16 + k] = (uint8_t)(dim >> (8 * k));
-                h[20] = (uint8_t)(a.bitwidth ? a.bitwidth : DS_FP32_TAG);
-                h[21] = (uint8_t)(a.bitwidth ? 1 : 0);
-                h[22] = (uint8_t)(a.aux ? 1 : 0);
-                h[23] = 0;
-            }
-            off += DS_HEADER_SIZE;
-        }
-        off += n * (int64_t)a.rec;
-        tiles += (n + a.tile_rows - 1) / a.tile_rows;
-    }
-    a.sched[nt] = tiles;
-    a.sec_off[nt] = off;
-    if (off > a.capacity) atomicOr(a.flags, DS_FLAG_CAPACITY);
-}
-
-// deterministic final error sum: writer CTAs in order, then fixup CTAs
-__global__ void err_reduce_kernel(const double *partials, int n, const double *partials_fix,
-                                  int nfix, double *out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < n; i++) s += partials[i];
-        for (int i = 0; i < nfix; i++) s += partials_fix[i];
-        *out = s;
-    }
-}
 
 // warp-tiles of the MODE 0/1 writer for `rows` records of dim `dim`
 static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
@@ -72,12 +24,11 @@ extern "C" int64_t ds_record_size(int64_t dim, int bitwidth, int aux, int increm
     return s;
 }
 
-static size_t ws_head_bytes() {
-    return (size_t)(3 * DS_MAX_TABLES + 4) * sizeof(int64_t) + (size_t)2 * 4096 * sizeof(double);
-}
+// workspace: [done counter, 16 B] [4096 error partials] [fixup masks]
+static size_t ws_head_bytes() { return 16 + (size_t)4096 * sizeof(double); }
 
 extern "C" size_t ds_writer_workspace_size(int ntables, int64_t max_rows, int64_t dim) {
-    // schedule + 2 x 4096 error partials + one fixup mask word per warp-tile
+    // done counter + 4096 error partials + one fixup mask word per warp-tile
     int64_t tiles = warp_tiles(max_rows > 0 ? max_rows : 0, ntables, dim > 0 ? dim : 1);
     return ws_head_bytes() + (size_t)tiles * sizeof(uint32_t) + 256;
 }
@@ -132,10 +83,10 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     a.aux_off = bw ? a.code_off + a.packed : a.par_off + 4 * d;
     a.ids = ids;
     a.counts = p->incremental ? counts : nullptr;
-    a.sched = reinterpret_cast<int64_t *>(workspace);
-    a.partials = reinterpret_cast<double *>(a.sched + 3 * DS_MAX_TABLES + 4);
-    a.partials_fix = a.partials + 4096;
-    a.fix_mask = reinterpret_cast<uint32_t *>(a.partials_fix + 4096);
+    a.done = reinterpret_cast<unsigned *>(workspace);
+    a.partials = reinterpret_cast<double *>(static_cast<uint8_t *>(workspace) + 16);
+    a.fix_mask = reinterpret_cast<uint32_t *>(a.partials + 4096);
+    a.err_out = err_sum;
     a.ids_packed = p->ids_packed;
     a.ids_local = p->ids_local;
     a.sec_off = sec_off;
@@ -188,12 +139,7 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     if (grid < 1) grid = 1;
     if (grid > 4096) grid = 4096;
 
-    cudaStream_t s = (cudaStream_t)stream;
-    layout_kernel<<<1, 32, 0, s>>>(a);
-    fn<<<(unsigned)grid, WT, smem, s>>>(a);
-    int st = host::check_launch("ds_write_payload");
-    if (st) return st;
-    int nfix = 0;
-    if (err_sum) err_reduce_kernel<<<1, 32, 0, s>>>(a.partials, (int)grid, a.partials_fix, nfix, err_sum);
-    return host::check_launch("ds_write_payload(err)");
+    // one launch: layout, records, exact fixups and the error sum
+    fn<<<(unsigned)grid, WT, smem, (cudaStream_t)stream>>>(a);
+    return host::check_launch("ds_write_payload");
 }

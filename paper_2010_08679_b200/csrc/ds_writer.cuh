@@ -45,12 +45,12 @@ struct WriterArgs {
     int ids_local;
     const int64_t *ids;
     const int64_t *counts;  // device per-table counts (incremental) or null
-    int64_t *sched;         // [0..nt] tile prefix, [nt+1..2nt] row counts, [2nt+1..3nt] ids offsets
-    int64_t *sec_off;       // [nt+1] section offsets + total
+    int64_t *sec_off;       // [nt+1] section offsets + total (written by CTA 0)
     uint8_t *payload;
     int64_t capacity;
-    double *partials;
-    double *partials_fix;  // per-CTA error of the rows re-coded by the fixup pass
+    double *partials;       // per-CTA error partials
+    double *err_out;        // final error sum (may be null)
+    unsigned *done;         // CTAs finished (last one reduces; zero between calls)
     uint32_t *fix_mask;    // MODE 1: per warp-tile mask of rows for the fixup pass
     uint32_t *flags;
     unsigned long long *stats;
@@ -312,8 +312,74 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
     return fix;
 }
 
-// block-level epilogue: error partial (deterministic final sum in
-// err_reduce_kernel), flags, diagnostics
+// ---------------------------------------------------------------------------
+// layout (payload.py:84-104): every CTA derives the section offsets and the
+// tile schedule from the device counts with one warp scan (no layout launch);
+// CTA 0 publishes sec_off, the 24-byte headers (payload.py:88-91) and the
+// capacity flag.  s_sched: [0..nt] tile prefix, [nt+1..2nt] row counts,
+// [2nt+1..3nt] ids offsets; s_sec: [0..nt] section offsets + total.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void writer_layout(const WriterArgs &a, int64_t *s_sched, int64_t *s_sec) {
+    const int nt = a.ntables;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int64_t tiles0 = 0, ids0 = 0, off0 = 0;  // carried across 32-table blocks
+        for (int b = 0; b < nt; b += 32) {
+            const int t = b + lane;
+            int64_t n = 0, tl = 0, by = 0;
+            if (t < nt) {
+                n = a.counts ? a.counts[t] : a.t[t].rows;
+                tl = (n + a.tile_rows - 1) / a.tile_rows;
+                by = (a.write_headers ? DS_HEADER_SIZE : 0) + n * (int64_t)a.rec;
+            }
+            int64_t it = tl, ii = n, io = by;  // inclusive scans
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t u = __shfl_up_sync(DS_FULL_MASK, it, o);
+                const int64_t v = __shfl_up_sync(DS_FULL_MASK, ii, o);
+                const int64_t w = __shfl_up_sync(DS_FULL_MASK, io, o);
+                if (lane >= o) { it += u; ii += v; io += w; }
+            }
+            if (t < nt) {
+                s_sched[t] = tiles0 + it - tl;
+                s_sched[nt + 1 + t] = n;
+                s_sched[2 * nt + 1 + t] = a.ids_packed ? ids0 + ii - n : a.t[t].ids_off;
+                s_sec[t] = off0 + io - by;
+            }
+            tiles0 += __shfl_sync(DS_FULL_MASK, it, 31);
+            ids0 += __shfl_sync(DS_FULL_MASK, ii, 31);
+            off0 += __shfl_sync(DS_FULL_MASK, io, 31);
+        }
+        if (lane == 0) {
+            s_sched[nt] = tiles0;
+            s_sec[nt] = off0;
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        const int64_t total = s_sec[nt];
+        for (int t = threadIdx.x; t <= nt; t += blockDim.x) a.sec_off[t] = s_sec[t];
+        if (threadIdx.x == 0 && total > a.capacity) atomicOr(a.flags, DS_FLAG_CAPACITY);
+        if (a.write_headers && total <= a.capacity) {
+            for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+                uint8_t *h = a.payload + s_sec[t];
+                const uint32_t tid = a.t[t].table_id, dim = a.t[t].dim;
+                const uint64_t n = (uint64_t)s_sched[nt + 1 + t];
+                h[0] = 'C'; h[1] = 'N'; h[2] = 'R'; h[3] = '1';
+                for (int k = 0; k < 4; k++) h[4 + k] = (uint8_t)(tid >> (8 * k));
+                for (int k = 0; k < 8; k++) h[8 + k] = (uint8_t)(n >> (8 * k));
+                for (int k = 0; k < 4; k++) h[16 + k] = (uint8_t)(dim >> (8 * k));
+                h[20] = (uint8_t)(a.bitwidth ? a.bitwidth : DS_FP32_TAG);
+                h[21] = (uint8_t)(a.bitwidth ? 1 : 0);
+                h[22] = (uint8_t)(a.aux ? 1 : 0);
+                h[23] = 0;
+            }
+        }
+    }
+}
+
+// block-level epilogue: error partial, flags, diagnostics; the last CTA to
+// finish sums the partials in CTA order (deterministic) into err_out
 __device__ __forceinline__ void writer_epilogue(const WriterArgs &a, WAcc &acc, double *s_red) {
     const int lane = threadIdx.x & 31;
     for (int o = 16; o > 0; o >>= 1) acc.err += __shfl_xor_sync(DS_FULL_MASK, acc.err, o);
@@ -334,10 +400,25 @@ __device__ __forceinline__ void writer_epilogue(const WriterArgs &a, WAcc &acc, 
         }
     }
     __syncthreads();
+    __shared__ bool s_last;
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < WT / 32; w++) s += s_red[w];
         a.partials[blockIdx.x] = s;
+        __threadfence();
+        s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x < 32) {
+        __threadfence();
+        // lane l sums partials l, l+32, ... in order; then a fixed shuffle tree
+        double s = 0.0;
+        for (int i = lane; i < (int)gridDim.x; i += 32) s += __ldcg(a.partials + i);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(DS_FULL_MASK, s, o);
+        if (lane == 0) {
+            if (a.err_out) *a.err_out = s;
+            *a.done = 0u;  // ready for the next call on this workspace
+        }
     }
 }
 
@@ -362,7 +443,8 @@ __device__ __forceinline__ int tile_table(const int64_t *s_sched, int nt, int64_
 // payload; the rows' exact errors are added (the hot loop left them out).
 // ---------------------------------------------------------------------------
 template <int G, int C, int VEC, bool PAD>
-__device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_sched, int64_t tile,
+__device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_sched,
+                                         const int64_t *s_sec, int64_t tile,
                                          unsigned m, uint8_t *cs_warp, int d, WAcc &acc) {
     using Lay = Layout<G, C, VEC>;
     constexpr int EPL = C * VEC;
@@ -438,7 +520,7 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
                        (rq.mode == 2 || !(sf > 0.0) ? 0.0 : sf * rsqrt(sf));
         __syncwarp();
         if (row_changed) {  // overwrite the record's packed codes (LSB-first bitstream)
-            uint8_t *pk = a.payload + a.sec_off[t] + (a.write_headers ? DS_HEADER_SIZE : 0) +
+            uint8_t *pk = a.payload + s_sec[t] + (a.write_headers ? DS_HEADER_SIZE : 0) +
                           (i0 + slot) * a.rec + a.code_off;
             const int N = a.bitwidth;
             for (int b = lig; b < a.packed; b += G) {
@@ -491,10 +573,10 @@ __global__ void __launch_bounds__(WT, 3) writer_warp_kernel(const WriterArgs a) 
     __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
     __shared__ double s_red[WT / 32];
     const int nt = a.ntables;
-    for (int k = threadIdx.x; k < 3 * nt + 1; k += WT) s_sched[k] = a.sched[k];
-    __syncthreads();
+    __shared__ int64_t s_sec[DS_MAX_TABLES + 1];
+    writer_layout(a, s_sched, s_sec);
     WAcc acc;
-    if (a.sec_off[nt] <= a.capacity) {  // else flagged by the layout kernel
+    if (s_sec[nt] <= a.capacity) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
         const int64_t total_tiles = s_sched[nt];
         const int64_t gw = (int64_t)blockIdx.x * (WT / 32) + wid;
         const int64_t nwarps = (int64_t)gridDim.x * (WT / 32);
@@ -599,7 +681,7 @@ __global__ void __launch_bounds__(WT, 3) writer_warp_kernel(const WriterArgs a) 
             const unsigned fixm = __ballot_sync(DS_FULL_MASK, fix && lig == 0);
             if (MODE == 1 && lane == 0) a.fix_mask[gw + (int64_t)k * nwarps] = fixm;
             __syncwarp();
-            const int64_t dst = a.sec_off[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
+            const int64_t dst = s_sec[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
             copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec, lane, 32);
             __syncwarp();  // the stage is rewritten by the next tile
             cur = nxt;
@@ -611,7 +693,7 @@ __global__ void __launch_bounds__(WT, 3) writer_warp_kernel(const WriterArgs a) 
             __syncwarp();
             for (int64_t tile = gw; tile < total_tiles; tile += nwarps) {
                 const unsigned m = a.fix_mask[tile];
-                if (m) fix_tile<G, C, VEC, PAD>(a, s_sched, tile, m, codes, d, acc);
+                if (m) fix_tile<G, C, VEC, PAD>(a, s_sched, s_sec, tile, m, codes, d, acc);
             }
         }
     }
@@ -637,13 +719,13 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
     __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
     __shared__ double s_red[WT / 32];
     const int nt = a.ntables;
-    for (int k = threadIdx.x; k < 3 * nt + 1; k += WT) s_sched[k] = a.sched[k];
-    __syncthreads();
+    __shared__ int64_t s_sec[DS_MAX_TABLES + 1];
+    writer_layout(a, s_sched, s_sec);
     WAcc acc;
     const int lane = threadIdx.x & 31;
     const int lig = lane & (G - 1);
     const int slot = threadIdx.x / G;
-    if (a.sec_off[nt] <= a.capacity) {  // else flagged by the layout kernel
+    if (s_sec[nt] <= a.capacity) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
         const int64_t total_tiles = s_sched[nt];
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const int t = tile_table(s_sched, nt, tile, lane);
@@ -678,7 +760,7 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
                                                d, acc);
             }
             __syncthreads();
-            const int64_t dst = a.sec_off[t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
+            const int64_t dst = s_sec[t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
             copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec, threadIdx.x, WT);
             __syncthreads();
         }

@@ -127,7 +127,7 @@ class ShardWriter:
         self.params.stats = None if stats is None else stats.data_ptr()
         self.write_headers = write_headers
         ws = int(self.L.ds_writer_workspace_size(len(tables), sum(t.rows for t in tables), self.dim))
-        self._ws = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        self._ws = torch.zeros(ws, dtype=torch.uint8, device=self.device)  # zero before first use
         self.sec_off = torch.zeros(len(tables) + 1, dtype=torch.int64, device=self.device)
         self.err = torch.zeros(1, dtype=torch.float64, device=self.device)
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.device)
