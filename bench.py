@@ -346,7 +346,10 @@ def run_ours(args):
     # (d=16, 8-bit: pick_cfg -> G=1 lane per row, C=4 x float4, naive mode 1)
     roofline = {"bound": "hbm", "kernel": {"mark": "ds::mark_tma_kernel<int>",
                                            "write": "ds::writer_warp_kernel<1,4,4,1,false>"}[dom],
-                "measured_over": "layout + writer + err_reduce launches of the write phase",
+                "measured_over": {"mark": "the mark phase (one mark_tma launch per step)",
+                                  "write": "the write phase (one writer launch per step)"}[dom],
+                "traffic_source": "profiles/traffic.json: dram read+write bytes per launch, "
+                                  "ncu --set full",
                 "achieved": phases[dom]["GB/s"], "peak": peak, "unit": "GB/s",
                 "frac": phases[dom]["GB/s"] / peak, "traffic": traffic,
                 "peak_source": peak_src}
