@@ -68,10 +68,11 @@ def workload_desc(cards, n_lookups_per_table):
         "tables": len(cards), "rows_per_rank": int(sum(cards)), "dim": DIM,
         "bitwidth": BITWIDTH, "batches_per_interval": BATCHES, "batch": BATCH,
         "lookups_per_step_per_rank": int(n_lookups_per_table * len(cards)),
-        "lookup_dtype": "int32", "scope": "interval (consecutive increments)",
+        "lookup_dtype": "per table: u8 (<=256 rows), u16 (<=65536), i32 (above)",
+        "scope": "interval (consecutive increments)",
         "row_map": "Zipf rank -> row through a seeded permutation per table",
         "l2": "flushed between timed steps (256 MB write; L2 126 MB); inputs 2.16 GB tables "
-              "+ 107 MB lookups per step and rank",
+              "+ a 61 MB packed lookup stream per step and rank",
     }
 
 
@@ -200,6 +201,20 @@ class CpuPath:
         return rows, sum(len(o[0]) for o in outs)
 
 
+def pack_lookups_device(lookups, cards, dev):
+    """Device LookupStream of per-table id tensors at each table's narrowest width."""
+    import torch
+    from paper_2010_08679_b200.tracker import LookupStream
+    boff, cnt, wid, tids, total = LookupStream.layout(dict(enumerate(cards)),
+                                                      {t: lk.numel() for t, lk in enumerate(lookups)})
+    buf = torch.zeros(max(16, total), dtype=torch.uint8, device=dev)
+    for t, (o, n, w) in enumerate(zip(boff, cnt, wid)):
+        x = lookups[t].to(torch.int64)
+        parts = [((x >> (8 * k)) & 0xFF).to(torch.uint8) for k in range(w)]
+        buf[o:o + n * w] = torch.stack(parts, dim=1).reshape(-1)
+    return LookupStream(buf, boff, cnt, wid, tids)
+
+
 # --------------------------------------------------------------------------------
 
 def run_reference(args):
@@ -241,7 +256,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2010_08679_b200 as ds
-    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer, gather_counts
+    from paper_2010_08679_b200.tracker import LookupStream
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,9 +280,9 @@ def run_ours(args):
         v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
         tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
     lookups = [zipf_lookups_torch(r, n_look, gen, dev) for r in cards]
-    idx = torch.cat(lookups)
-    seg_off = np.arange(len(cards) + 1, dtype=np.int64) * n_look
-    seg_tab = np.arange(len(cards))
+    # the interval's lookup stream, each table at its narrowest id width
+    # (u8 <= 256 rows, u16 <= 65536, i32 above): ds_mark_packed's input
+    stream = pack_lookups_device(lookups, cards, dev)
     ck = ShardedCheckpointer(tables, BITWIDTH, rank=rank, world_size=world, device=dev)
     torch.cuda.synchronize()
 
@@ -283,11 +299,11 @@ def run_ours(args):
 
     # warm-up: W steps, then keep stepping until the clocks have ramped (>= 0.3 s)
     for _ in range(max(3, args.warmup)):
-        ck.step(idx, seg_off, seg_tab)
+        ck.step(stream)
     torch.cuda.synchronize()
     t_end = time.perf_counter() + 0.3
     while time.perf_counter() < t_end:
-        ck.step(idx, seg_off, seg_tab)
+        ck.step(stream)
         torch.cuda.synchronize()
     ck.fetch()  # raises any flagged data error of the warm-up steps
 
@@ -297,6 +313,8 @@ def run_ours(args):
     # of the per-step event intervals (the flush itself is not timed).
     K = args.steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    main = torch.cuda.current_stream(dev)
+    comm = torch.cuda.Stream(dev)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     barrier()
     torch.cuda.synchronize()
@@ -304,13 +322,17 @@ def run_ours(args):
         for k in range(K):
             flush.fill_(k & 0xFF)
             ev[k][0].record()
-            ck.mark(idx, seg_off, seg_tab)                 # K1
+            ck.mark(stream)                                # K1
             ev[k][1].record()
             ck.tracker.capture_into(ck.ids, ck.counts, fold=1, scope=ck.scope)   # K2
-            if world > 1:
-                dist.all_gather_into_tensor(ck.all_counts, ck.counts)
             ev[k][2].record()
+            if world > 1:  # count all_gather on a side stream, overlapped with K3
+                comm.wait_stream(main)
+                with torch.cuda.stream(comm):
+                    gather_counts(ck.counts, world, out=ck.all_counts)
             ck.writer.write(ck.payload, ck.ids, ck.counts[:ck.nt], None, local_ids=True)  # K3
+            if world > 1:
+                main.wait_stream(comm)
             ev[k][3].record()
         torch.cuda.synchronize()
     barrier()
@@ -327,7 +349,7 @@ def run_ours(args):
 
     # roofline of the dominant kernel (algorithmic bytes / its mean duration)
     rec = ck.rec
-    k1_bytes = n_look * len(cards) * 4
+    k1_bytes = stream.nbytes
     k3_bytes = dirty_rank * (row_bytes + 8 + rec) + len(cards) * 24
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -363,17 +385,18 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         from paper_2010_08679_b200.pipeline import CheckpointPipeline
-        idx_host = idx.cpu().pin_memory()
-        pipe = CheckpointPipeline(ck, idx.numel(), idx.dtype)
+        host_stream = LookupStream(stream.buf.cpu().pin_memory(), stream.seg_byte_off,
+                                   stream.seg_count, stream.seg_width, stream.seg_tables)
+        pipe = CheckpointPipeline(ck, host_stream.nbytes, torch.uint8)
         for _ in range(3):
-            pipe.submit(idx_host, seg_off, seg_tab)
+            pipe.submit(host_stream)
         pipe.drain()
         h2d0, d2h0 = pipe.h2d_bytes, pipe.d2h_bytes
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(K):
-            pipe.submit(idx_host, seg_off, seg_tab)
+            pipe.submit(host_stream)
         pipe.drain()
         e_el = max_over_ranks(time.perf_counter() - t0)
         barrier()

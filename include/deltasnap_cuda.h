@@ -91,6 +91,18 @@ DS_API int ds_mark_i32(uint32_t *words, const int64_t *word_off_host, const int6
                        const int32_t *idx, const int64_t *seg_off_host,
                        const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream);
 
+/* Packed mixed-width lookup stream: segment s holds seg_count[s] ids of
+ * seg_width[s] bytes (1 and 2: unsigned; 4 and 8: signed two's complement)
+ * starting at byte seg_byte_off[s] of `lookups` (16-byte aligned, as is
+ * `lookups`), all marking table seg_table[s].  Sending each table's ids at
+ * the narrowest width its row count allows (u8 <= 256 rows, u16 <= 65536)
+ * cuts the lookup bytes the end-to-end path moves over PCIe and K1 streams
+ * from HBM.  Same bit semantics and DS_FLAG_BOUNDS behaviour as ds_mark. */
+DS_API int ds_mark_packed(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+                          const void *lookups, const int64_t *seg_byte_off_host,
+                          const int64_t *seg_count_host, const int32_t *seg_width_host,
+                          const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream);
+
 /* Single-table convenience form (DirtyBitmap.mark). */
 DS_API int ds_mark_table(uint32_t *words, int64_t rows, const int64_t *idx, int64_t n, uint32_t *flags,
                   void *stream);

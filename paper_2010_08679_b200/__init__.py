@@ -19,7 +19,7 @@ from .errors import (
     StoreConflictError,
     StoreIOError,
 )
-from .tracker import DirtyBitmap, ModelTracker, TrackerView
+from .tracker import DirtyBitmap, LookupStream, ModelTracker, TrackerView, lookup_width
 from .quant import (
     AdaptiveConfig,
     QuantParams,

@@ -81,6 +81,7 @@ _SIGNATURES = {
     "ds_get_l2_fetch_granularity": (_I, []),
     "ds_mark": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P]),
     "ds_mark_i32": (_I, [_P, _P, _P, _P, _P, _P, _I, _P, _P]),
+    "ds_mark_packed": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P]),
     "ds_mark_table": (_I, [_P, _I64, _P, _I64, _P, _P]),
     "ds_bitmap_op": (_I, [_P, _P, _P, _I64, _I, _P]),
     "ds_popcount": (_I, [_P, _I64, _P, _P]),

@@ -39,6 +39,10 @@ inline bool env_flag(const char *name) {
     const char *v = getenv(name);
     return v && v[0] && v[0] != '0';
 }
+inline int64_t env_int(const char *name, int64_t dflt) {
+    const char *v = getenv(name);
+    return v && v[0] ? strtoll(v, nullptr, 10) : dflt;
+}
 
 // Grid for a grid-stride kernel: enough blocks to cover n, capped at
 // `per_sm` resident blocks per SM.

@@ -25,7 +25,13 @@ struct MarkArgs {
     int64_t rows[DS_MAX_TABLES];
     int64_t seg_off[DS_MAX_TABLES + 1];
     int32_t seg_table[DS_MAX_TABLES];
-    int blk_off[DS_MAX_TABLES + 1];  // TMA kernel: first CTA of each segment
+    int blk_off[DS_MAX_TABLES + 1];  // TMA kernel: first CTA of the j-th segment of seg_order
+    int32_t seg_order[DS_MAX_TABLES];  // TMA kernel: segments, most expensive kind first
+    int64_t seg_pb[DS_MAX_TABLES];     // TMA kernel: lookups per CTA of each segment
+    const uint8_t *ibytes;             // TMA kernel: packed lookup stream
+    int64_t seg_boff[DS_MAX_TABLES];   // TMA kernel: byte offset of each segment (16-aligned)
+    int64_t seg_n[DS_MAX_TABLES];      // TMA kernel: ids in each segment
+    int32_t seg_width[DS_MAX_TABLES];  // TMA kernel: bytes per id (1, 2 unsigned; 4, 8 signed)
     int nseg;
 };
 
@@ -160,8 +166,6 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_kernel(const MarkArgs a, in
 // bit.  Correct for any interleaving: bits are only ever set, and a cache
 // entry only claims bits this CTA has itself OR-ed (or seen OR-ed) into HBM.
 // ---------------------------------------------------------------------------
-constexpr int MK_STAGES = 4;
-constexpr int MK_STAGE_BYTES = 8192;  // 2048 int32 ids: 8 per thread
 constexpr int MK_CACHE_BITS = 11;      // 2048 entries (16 KB)
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -196,56 +200,69 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 }
 
 // Every CTA works inside ONE segment (one table's slice of the lookup
-// stream); the host gives each segment ceil(len / per_block) CTAs.
-//  * small tables (bitmap <= MK_WIN_WORDS words): the CTA ORs into a
-//    shared-memory copy of the table's bitmap (ATOMS, no HBM traffic) and at
-//    the end ORs each non-zero word into HBM once (RED);
-//  * large tables: shared cache of (word, bits known set) with second-chance
-//    replacement; a miss issues one RED.OR (fire and forget).
+// stream) and each of its warps runs its own TMA ring over every 8th chunk of
+// the CTA's range (no CTA barrier in the loop).  Per table size:
+//  * rows <= MK_BYTE_ROWS (all 18 small Criteo-Kaggle tables): a shared
+//    byte per row; a lookup is one plain byte store (racing stores all write
+//    1, so no atomics and no read), folded into bitmap words and OR-ed into HBM
+//    once per CTA at the end;
+//  * rows <= 32 * MK_WIN_WORDS: a shared copy of the bitmap words
+//    (read-before-ATOMS: hot words are already set and same-address reads
+//    broadcast), flushed with one RED per touched word;
+//  * larger: a shared cache of (word, bits known set) with second-chance
+//    replacement; a miss issues one fire-and-forget RED.OR.
 // Correct for any interleaving: bits are only ever set, and a cache entry
 // only claims bits this CTA itself OR-ed into HBM.
-constexpr int MK_WIN_WORDS = 2048;  // 65536 rows: 18 of the 26 Criteo-Kaggle tables
+constexpr int MK_WIN_WORDS = 2048;   // 65536 rows
+constexpr int MK_BYTE_ROWS = 16384 - 32;  // byte map + one dummy byte in the 16 KB cache
+constexpr int MK_WSTAGES = 4;        // per-warp ring depth
+constexpr int MK_WSTAGE_BYTES = 1024;  // per-warp stage: 256 int32 / 128 int64 ids
+constexpr int MK_WARPS = MARK_THREADS / 32;
 
+// One CTA's range [start, end) (ids of segment `seg`, width sizeof(IdxT)).
 template <typename IdxT>
-__global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a, int64_t per_block,
-                                                               int unused) {
-    constexpr int IDS = MK_STAGE_BYTES / (int)sizeof(IdxT);  // ids per stage
-    constexpr int PER_THREAD = IDS / MARK_THREADS;            // 8 (int32) or 4 (int64)
-    extern __shared__ __align__(128) uint8_t mk_smem[];
-    IdxT *buf = reinterpret_cast<IdxT *>(mk_smem);
-    __shared__ __align__(8) unsigned long long bars[MK_STAGES];
-    __shared__ unsigned long long cache[1 << MK_CACHE_BITS];  // large tables
-    uint32_t *win = reinterpret_cast<uint32_t *>(cache);      // small tables (aliases the cache)
-    static_assert(MK_WIN_WORDS * 4 <= (1 << MK_CACHE_BITS) * 8, "window must fit the cache");
-    // segment of this CTA: last s with blk_off[s] <= blockIdx.x
-    int seg = 0;
-    while (seg + 1 < a.nseg && a.blk_off[seg + 1] <= (int)blockIdx.x) seg++;
-    const int64_t s0 = a.seg_off[seg], s1 = a.seg_off[seg + 1];
-    const int64_t start = s0 + (int64_t)(blockIdx.x - a.blk_off[seg]) * per_block;
-    const int64_t end = min(s1, start + per_block);
-    const uint32_t base = (uint32_t)a.word_off[a.seg_table[seg]];
-    const uint64_t rows = (uint64_t)a.rows[a.seg_table[seg]];
+__device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t start, int64_t end,
+                                           unsigned long long *cache,
+                                           unsigned long long (*bars)[MK_WSTAGES], uint8_t *mk_smem) {
+    constexpr int IDS = MK_WSTAGE_BYTES / (int)sizeof(IdxT);  // ids per warp stage
+    constexpr int PER_LANE = IDS / 32;                          // 32 B of ids per lane
+    uint32_t *win = reinterpret_cast<uint32_t *>(cache);  // bit window (aliases the cache)
+    uint8_t *bytes = reinterpret_cast<uint8_t *>(cache);  // byte map (aliases the cache)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t base = (uint32_t)a.word_off[seg];
+    const uint64_t rows = (uint64_t)a.rows[seg];
     const uint32_t nwords = (uint32_t)((rows + 31) / 32);
-    const bool small = nwords <= (uint32_t)MK_WIN_WORDS;
+    // 32-bit bound for the byte map (int32 ids never exceed 2^31 - 1)
+    const uint32_t rows32 = (uint32_t)min(rows, (uint64_t)0x80000000ull);
+    auto in_range = [&](IdxT v) -> bool {  // negatives wrap high
+        if (sizeof(IdxT) <= 4) return (uint32_t)v < rows32;
+        return (uint64_t)(int64_t)v < rows;
+    };
+    const int mode = rows <= (uint64_t)MK_BYTE_ROWS ? 0 : (nwords <= (uint32_t)MK_WIN_WORDS ? 1 : 2);
     for (int k = threadIdx.x; k < (1 << MK_CACHE_BITS); k += MARK_THREADS) cache[k] = 0ull;
-    const IdxT *idx = static_cast<const IdxT *>(a.idx);
+    const IdxT *idx = reinterpret_cast<const IdxT *>(a.ibytes + a.seg_boff[seg]);
+    IdxT *ring = reinterpret_cast<IdxT *>(mk_smem) + (size_t)wid * MK_WSTAGES * IDS;
+    unsigned long long *wb = bars[wid];
     // TMA moves whole 16-byte units; the ragged tail (< 16 B) is read directly
     const int64_t bulk_end =
         start + ((end - start) * (int64_t)sizeof(IdxT) / 16) * 16 / (int64_t)sizeof(IdxT);
     const int nch = (int)((bulk_end - start + IDS - 1) / IDS);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < MK_STAGES; s++) mbar_init(&bars[s], 1);
+    if (lane == 0) {
+        for (int s = 0; s < MK_WSTAGES; s++) mbar_init(&wb[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < MK_STAGES && k < nch; k++) {
-            int64_t c0 = start + (int64_t)k * IDS;
-            unsigned bytes = (unsigned)(min((int64_t)IDS, bulk_end - c0) * sizeof(IdxT));
-            mbar_expect_tx(&bars[k], bytes);
-            tma_load_1d(buf + (size_t)k * IDS, idx + c0, bytes, &bars[k]);
+    __syncthreads();  // cache/map zeroed, barriers initialised
+    auto issue = [&](int k) {  // lane 0: chunk wid + 8k into stage k % STAGES
+        const int c = wid + k * MK_WARPS;
+        if (c < nch) {
+            const int64_t c0 = start + (int64_t)c * IDS;
+            const unsigned nb = (unsigned)(min((int64_t)IDS, bulk_end - c0) * sizeof(IdxT));
+            mbar_expect_tx(&wb[k % MK_WSTAGES], nb);
+            tma_load_1d(ring + (size_t)(k % MK_WSTAGES) * IDS, idx + c0, nb, &wb[k % MK_WSTAGES]);
         }
-    }
+    };
+    if (lane == 0)
+        for (int k = 0; k < MK_WSTAGES; k++) issue(k);
     bool bad = false;
     // Cache entry: key (word+1, 31 bits) << 33 | referenced << 32 | bits known
     // set.  Second-chance replacement keeps the Zipf head cached.
@@ -262,7 +279,9 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a
         else cache[slot] = ((unsigned long long)(w + 1) << 33) | bit;
     };
     auto mark_row = [&](uint32_t u) {
-        if (small) {
+        if (mode == 0) {
+            bytes[u] = 1;
+        } else if (mode == 1) {
             atomicOr(win + (u >> 5), 1u << (u & 31));  // shared-memory OR
         } else {
             const uint32_t w = base + (u >> 5);
@@ -270,65 +289,91 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a
             cache_mark(w, 1u << (u & 31), slot, cache[slot]);
         }
     };
-    for (int k = 0; k < nch; k++) {
-        const int s = k % MK_STAGES;
-        mbar_wait(&bars[s], (unsigned)(k / MK_STAGES) & 1u);
-        const int64_t c0 = start + (int64_t)k * IDS;
+    for (int k = 0;; k++) {
+        const int c = wid + k * MK_WARPS;
+        if (c >= nch) break;
+        const int s = k % MK_WSTAGES;
+        mbar_wait(&wb[s], (unsigned)(k / MK_WSTAGES) & 1u);
+        const int64_t c0 = start + (int64_t)c * IDS;
         const int cnt = (int)min((int64_t)IDS, bulk_end - c0);
-        const IdxT *b = buf + (size_t)s * IDS;
-        const int j0 = threadIdx.x * PER_THREAD;
-        if (j0 + PER_THREAD <= cnt) {
-            IdxT v[PER_THREAD];
+        const IdxT *b = ring + (size_t)s * IDS;
+        const int j0 = lane * PER_LANE;
+        if (j0 + PER_LANE <= cnt) {
+            // two 16-byte halves per lane (keeps the live ids few)
+            constexpr int PH = PER_LANE / 2;
 #pragma unroll
-            for (int q = 0; q < PER_THREAD * (int)sizeof(IdxT) / 16; q++)
-                reinterpret_cast<int4 *>(v)[q] = reinterpret_cast<const int4 *>(b + j0)[q];
-            if (small) {
-                // read first: hot words are already set and same-address reads
-                // broadcast, while same-address shared atomics serialise
-                uint32_t cur[PER_THREAD];
-                bool ok[PER_THREAD];
+            for (int h = 0; h < 2; h++) {
+                IdxT v[PH];
+                *reinterpret_cast<int4 *>(v) = reinterpret_cast<const int4 *>(b + j0)[h];
+                if (mode == 0) {
+                    // out-of-range ids store to the dummy byte at index `rows`
+                    // (masked off by the flush) instead of branching
+                    const uint32_t sb = smem_u32(bytes);
+                    if (sizeof(IdxT) <= 4) {
+                        uint32_t umax = 0;  // negatives wrap high
 #pragma unroll
-                for (int q = 0; q < PER_THREAD; q++) {
-                    ok[q] = (uint64_t)(int64_t)v[q] < rows;  // negatives wrap high
-                    bad |= !ok[q];
-                    cur[q] = ok[q] ? win[(uint32_t)v[q] >> 5] : ~0u;
+                        for (int q = 0; q < PH; q++) {
+                            const uint32_t u = (uint32_t)v[q];
+                            umax = max(umax, u);
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + min(u, rows32)), "r"(1) : "memory");
+                        }
+                        bad |= umax >= rows32;
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < PH; q++) {
+                            const bool ok = in_range(v[q]);
+                            bad |= !ok;
+                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + (ok ? (uint32_t)v[q] : rows32)),
+                                         "r"(1) : "memory");
+                        }
+                    }
+                } else if (mode == 1) {
+                    uint32_t cur[PH];
+                    bool ok[PH];
+#pragma unroll
+                    for (int q = 0; q < PH; q++) {
+                        ok[q] = in_range(v[q]);
+                        bad |= !ok[q];
+                        cur[q] = ok[q] ? win[(uint32_t)v[q] >> 5] : ~0u;
+                    }
+#pragma unroll
+                    for (int q = 0; q < PH; q++) {
+                        const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
+                        if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
+                    }
+                } else {
+                    // probes in groups of 8 so their latencies overlap
+                    constexpr int PG = PH < 8 ? PH : 8;
+#pragma unroll
+                    for (int g = 0; g < PH; g += PG) {
+                        uint32_t w[PG], slot[PG];
+                        unsigned long long e[PG];
+                        bool ok[PG];
+#pragma unroll
+                        for (int q = 0; q < PG; q++) {
+                            ok[q] = in_range(v[g + q]);
+                            bad |= !ok[q];
+                            w[q] = base + ((uint32_t)v[g + q] >> 5);
+                            slot[q] = (w[q] * 2654435761u) >> (32 - MK_CACHE_BITS);
+                            e[q] = cache[slot[q]];
+                        }
+#pragma unroll
+                        for (int q = 0; q < PG; q++)
+                            if (ok[q]) cache_mark(w[q], 1u << ((uint32_t)v[g + q] & 31), slot[q], e[q]);
+                    }
                 }
-#pragma unroll
-                for (int q = 0; q < PER_THREAD; q++) {
-                    const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
-                    if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
-                }
-            } else {
-                // all cache probes before any update so their latencies overlap
-                uint32_t w[PER_THREAD], slot[PER_THREAD];
-                unsigned long long e[PER_THREAD];
-                bool ok[PER_THREAD];
-#pragma unroll
-                for (int q = 0; q < PER_THREAD; q++) {
-                    ok[q] = (uint64_t)(int64_t)v[q] < rows;
-                    bad |= !ok[q];
-                    w[q] = base + ((uint32_t)v[q] >> 5);
-                    slot[q] = (w[q] * 2654435761u) >> (32 - MK_CACHE_BITS);
-                    e[q] = cache[slot[q]];
-                }
-#pragma unroll
-                for (int q = 0; q < PER_THREAD; q++)
-                    if (ok[q]) cache_mark(w[q], 1u << ((uint32_t)v[q] & 31), slot[q], e[q]);
             }
         } else {
-            for (int q = j0; q < cnt && q < j0 + PER_THREAD; q++) {
+            for (int q = j0; q < cnt && q < j0 + PER_LANE; q++) {
                 const int64_t r = (int64_t)b[q];
                 if ((uint64_t)r >= rows) bad = true;
                 else mark_row((uint32_t)r);
             }
         }
-        __syncthreads();  // every thread is done with stage s
-        if (threadIdx.x == 0 && k + MK_STAGES < nch) {
+        __syncwarp();  // every lane is done with stage s
+        if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            int64_t c1 = start + (int64_t)(k + MK_STAGES) * IDS;
-            unsigned bytes = (unsigned)(min((int64_t)IDS, bulk_end - c1) * sizeof(IdxT));
-            mbar_expect_tx(&bars[s], bytes);
-            tma_load_1d(buf + (size_t)s * IDS, idx + c1, bytes, &bars[s]);
+            issue(k + MK_WSTAGES);
         }
     }
     // ragged tail
@@ -337,14 +382,52 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a
         if ((uint64_t)r >= rows) bad = true;
         else mark_row((uint32_t)r);
     }
-    if (small) {  // flush the window: one RED per touched word
+    if (mode != 2) {
         __syncthreads();
-        for (uint32_t k = threadIdx.x; k < nwords; k += MARK_THREADS) {
-            const uint32_t v = win[k];
-            if (v) atomicOr(a.words + base + k, v);
+        if (mode == 0) {  // byte map -> bitmap words: 32 bytes (0/1) per word
+            for (uint32_t k = threadIdx.x; k < nwords; k += MARK_THREADS) {
+                const uint4 *p = reinterpret_cast<const uint4 *>(bytes + 32 * k);
+                const uint4 u0 = p[0], u1 = p[1];
+                const uint32_t c8[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+                uint32_t v = 0;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t c = c8[q];
+                    v |= ((c & 1u) | ((c >> 7) & 2u) | ((c >> 14) & 4u) | ((c >> 21) & 8u)) << (4 * q);
+                }
+                if (k == nwords - 1 && (rows & 31)) v &= (1u << (rows & 31)) - 1u;  // dummy byte
+                if (v) atomicOr(a.words + base + k, v);
+            }
+        } else {
+            for (uint32_t k = threadIdx.x; k < nwords; k += MARK_THREADS) {
+                const uint32_t v = win[k];
+                if (v) atomicOr(a.words + base + k, v);
+            }
         }
     }
-    if (__any_sync(DS_FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
+    if (__any_sync(DS_FULL_MASK, bad) && lane == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
+}
+
+// Segments of 1-byte / 2-byte (unsigned) and 4-byte / 8-byte (signed) ids:
+// the host sends each table's lookups at the narrowest width its row count
+// allows, which is what bounds the end-to-end H2D of the lookup stream.
+__global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a) {
+    extern __shared__ __align__(128) uint8_t mk_smem[];
+    __shared__ __align__(8) unsigned long long bars[MK_WARPS][MK_WSTAGES];
+    __shared__ __align__(16) unsigned long long cache[1 << MK_CACHE_BITS];  // 16 KB
+    static_assert(MK_WIN_WORDS * 4 <= (1 << MK_CACHE_BITS) * 8, "window must fit the cache");
+    static_assert(MK_BYTE_ROWS + 32 <= (1 << MK_CACHE_BITS) * 8, "byte map must fit the cache");
+    int j = 0;  // position in seg_order: last j with blk_off[j] <= blockIdx.x
+    while (j + 1 < a.nseg && a.blk_off[j + 1] <= (int)blockIdx.x) j++;
+    const int seg = a.seg_order[j];
+    const int64_t start = (int64_t)(blockIdx.x - a.blk_off[j]) * a.seg_pb[seg];
+    const int64_t end = min(a.seg_n[seg], start + a.seg_pb[seg]);
+    switch (a.seg_width[seg]) {
+    case 1: mark_range<uint8_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 2: mark_range<uint16_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 4: mark_range<int32_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    default: mark_range<int64_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -958,11 +1041,121 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
 
 using namespace ds;
 
+// TMA form over a packed stream of segments (16-byte aligned, any width).
+// Lookups are weighted by the per-lookup cost of their table's kind (byte map
+// 1, bit window 2, cache + RED 3, measured on B200) and cut into CTAs of
+// about equal cost, expensive kinds first; every CTA range is a multiple of a
+// warp stage so every bulk copy starts 16-byte aligned.
+static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int64_t *rows,
+                            const void *lookups, const int64_t *seg_boff, const int64_t *seg_n,
+                            const int32_t *seg_width, const int32_t *seg_table_host, int nseg,
+                            uint32_t *flags, void *stream) {
+    if (nseg < 1 || nseg > DS_MAX_TABLES)
+        return host::fail(DS_ERR_ARG, "ds_mark_packed: nseg out of range");
+    if (!words || !word_off || !rows || !flags || !seg_boff || !seg_n || !seg_width)
+        return host::fail(DS_ERR_ARG, "ds_mark_packed: null pointer");
+    MarkArgs a;
+    a.words = words;
+    a.idx = lookups;
+    a.ibytes = static_cast<const uint8_t *>(lookups);
+    a.flags = flags;
+    a.nseg = nseg;
+    int64_t total = 0, max_word = 0;
+    for (int s = 0; s < nseg; s++) {
+        const int t = seg_table_host ? seg_table_host[s] : 0;
+        if (t < 0 || t >= DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark_packed: table index");
+        const int w = seg_width[s];
+        if (w != 1 && w != 2 && w != 4 && w != 8)
+            return host::fail(DS_ERR_ARG, "ds_mark_packed: id width must be 1, 2, 4 or 8 bytes");
+        if (seg_boff[s] % 16 || seg_n[s] < 0)
+            return host::fail(DS_ERR_ARG, "ds_mark_packed: segments must start 16-byte aligned");
+        a.word_off[s] = word_off[t];
+        a.rows[s] = rows[t];
+        a.seg_boff[s] = seg_boff[s];
+        a.seg_n[s] = seg_n[s];
+        a.seg_width[s] = w;
+        total += seg_n[s];
+        const int64_t mw = word_off[t] + (rows[t] + 31) / 32;
+        max_word = mw > max_word ? mw : max_word;
+    }
+    if (total == 0) return DS_OK;
+    if (!lookups || reinterpret_cast<uintptr_t>(lookups) % 16)
+        return host::fail(DS_ERR_ARG, "ds_mark_packed: lookups must be 16-byte aligned");
+    // the cache keys are 31-bit word ids
+    if (max_word >= (int64_t)0x7fffffffLL)
+        return host::fail(DS_ERR_CONFIG, "ds_mark: a table set holds at most 2^31-1 bitmap words");
+    const size_t smem = (size_t)MK_WARPS * MK_WSTAGES * MK_WSTAGE_BYTES;
+    auto fn = mark_tma_kernel;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
+    int tper = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, fn, MARK_THREADS, smem);
+    if (tper < 1) tper = 1;
+    static const int64_t kCost[3] = {1, 2, 3};
+    const int64_t cost_cache = host::env_int("DS_MARK_COST_CACHE", kCost[2]);
+    int kind[DS_MAX_TABLES];
+    double total_cost = 0.0;
+    for (int s = 0; s < nseg; s++) {
+        const int64_t r = a.rows[s];
+        kind[s] = r <= MK_BYTE_ROWS ? 0 : ((r + 31) / 32 <= MK_WIN_WORDS ? 1 : 2);
+        const int64_t w = kind[s] == 2 ? cost_cache : kCost[kind[s]];
+        total_cost += (double)a.seg_n[s] * (double)w;
+    }
+    const double waves = (double)host::env_int("DS_MARK_WAVES", 2);
+    const double target = total_cost / ((double)host::sm_count() * tper * waves);
+    int64_t nb = 0;
+    int j = 0;
+    for (int kd = 2; kd >= 0; kd--) {
+        for (int s = 0; s < nseg; s++) {
+            if (kind[s] != kd) continue;
+            const int64_t w = kd == 2 ? cost_cache : kCost[kd];
+            const int64_t ids_per_stage = MK_WSTAGE_BYTES / a.seg_width[s];
+            int64_t pb = (int64_t)(target / (double)w) + 1;
+            pb = (pb + ids_per_stage - 1) / ids_per_stage * ids_per_stage;
+            a.seg_pb[s] = pb;
+            a.seg_order[j] = s;
+            a.blk_off[j] = (int)nb;
+            nb += (a.seg_n[s] + pb - 1) / pb;
+            j++;
+        }
+    }
+    a.blk_off[nseg] = (int)nb;
+    if (nb == 0) return DS_OK;
+    fn<<<(unsigned)nb, MARK_THREADS, smem, (cudaStream_t)stream>>>(a);
+    return host::check_launch("ds_mark");
+}
+
 static int mark_impl(uint32_t *words, const int64_t *word_off, const int64_t *rows,
                      const void *idx, int idx32, const int64_t *seg_off_host,
                      const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream) {
     if (nseg < 1 || nseg > DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark: nseg out of range");
     if (!words || !word_off || !rows || !flags) return host::fail(DS_ERR_ARG, "ds_mark: null pointer");
+    const int64_t isz = idx32 ? 4 : 8;
+    int64_t total = seg_off_host[nseg] - seg_off_host[0];
+    if (total <= 0) return DS_OK;
+    if (!idx) return host::fail(DS_ERR_ARG, "ds_mark: null idx");
+    // TMA form when every segment starts 16-byte aligned
+    bool aligned = reinterpret_cast<uintptr_t>(idx) % 16 == 0;
+    for (int s = 0; s <= nseg; s++) aligned &= (seg_off_host[s] * isz) % 16 == 0;
+    int64_t max_word = 0;
+    for (int s = 0; s < nseg; s++) {
+        const int t = seg_table_host ? seg_table_host[s] : 0;
+        if (t < 0 || t >= DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark: table index");
+        const int64_t mw = word_off[t] + (rows[t] + 31) / 32;
+        max_word = mw > max_word ? mw : max_word;
+    }
+    if (aligned && max_word < (int64_t)0x7fffffffLL && !host::env_flag("DS_MARK_NO_TMA")) {
+        int64_t boff[DS_MAX_TABLES], n[DS_MAX_TABLES];
+        int32_t wd[DS_MAX_TABLES];
+        for (int s = 0; s < nseg; s++) {
+            boff[s] = seg_off_host[s] * isz;
+            n[s] = seg_off_host[s + 1] - seg_off_host[s];
+            wd[s] = (int32_t)isz;
+        }
+        return mark_packed_impl(words, word_off, rows, idx, boff, n, wd, seg_table_host, nseg, flags,
+                                stream);
+    }
+    // grid-stride form for unaligned streams
     MarkArgs a;
     a.words = words;
     a.idx = idx;
@@ -970,18 +1163,16 @@ static int mark_impl(uint32_t *words, const int64_t *word_off, const int64_t *ro
     a.flags = flags;
     a.nseg = nseg;
     for (int s = 0; s < nseg; s++) {
-        int t = seg_table_host ? seg_table_host[s] : 0;
-        if (t < 0 || t >= DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark: table index");
-        a.seg_table[s] = s;  // resolved below: per-segment base/rows
+        const int t = seg_table_host ? seg_table_host[s] : 0;
+        a.seg_table[s] = s;  // per-segment base/rows resolved here
         a.word_off[s] = word_off[t];
         a.rows[s] = rows[t];
         a.seg_off[s] = seg_off_host[s];
     }
     a.seg_off[nseg] = seg_off_host[nseg];
-    int64_t total = a.seg_off[nseg] - a.seg_off[0];
-    if (total <= 0) return DS_OK;
-    if (!idx) return host::fail(DS_ERR_ARG, "ds_mark: null idx");
-    // one contiguous, 8-aligned range per CTA; exactly one wave of resident CTAs
+    // word ids are 32-bit inside the kernel (and the cache keys are word+1)
+    if (max_word >= (int64_t)0xffffffffLL)
+        return host::fail(DS_ERR_CONFIG, "ds_mark: a table set holds at most 2^32-1 bitmap words");
     const int64_t quantum = (int64_t)MARK_THREADS * MARK_PER_THREAD;
     int per_sm = 0;
     if (idx32)
@@ -994,53 +1185,23 @@ static int mark_impl(uint32_t *words, const int64_t *word_off, const int64_t *ro
     int64_t per_block = (total + blocks - 1) / blocks;
     per_block = (per_block + quantum - 1) / quantum * quantum;
     blocks = (total + per_block - 1) / per_block;
-    const size_t isz = idx32 ? 4 : 8;
-    int vec = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) &&
-              ((a.seg_off[0] * (int64_t)isz) % 16 == 0);
-    int64_t max_word = 0;
-    for (int s = 0; s < nseg; s++) max_word = a.word_off[s] + (a.rows[s] + 31) / 32 > max_word
-                                                 ? a.word_off[s] + (a.rows[s] + 31) / 32 : max_word;
-    // word ids are 32-bit inside the kernel (and the cache keys are word+1)
-    if (max_word >= (int64_t)0xffffffffLL)
-        return host::fail(DS_ERR_CONFIG, "ds_mark: a table set holds at most 2^32-1 bitmap words");
-    int use_cache = 1;
-    // (the TMA kernel's cache keys are 31-bit word ids)
-    // every segment must start 16-byte aligned for the bulk copies
-    bool seg_aligned = true;
-    for (int s = 0; s <= nseg; s++) seg_aligned &= ((a.seg_off[s] * (int64_t)isz) % 16) == 0;
-    if (vec && seg_aligned && max_word < (int64_t)0x7fffffffLL && !host::env_flag("DS_MARK_NO_TMA")) {
-        // TMA-streamed form: CTAs never straddle a segment; each CTA's range
-        // is a multiple of a stage so every bulk copy starts 16-byte aligned
-        const int ids_per_stage = MK_STAGE_BYTES / (int)isz;
-        const size_t smem = (size_t)MK_STAGES * MK_STAGE_BYTES;
-        auto fn = idx32 ? (void (*)(const MarkArgs, int64_t, int))mark_tma_kernel<int32_t>
-                        : (void (*)(const MarkArgs, int64_t, int))mark_tma_kernel<int64_t>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
-        int tper = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, fn, MARK_THREADS, smem);
-        if (tper < 1) tper = 1;
-        int64_t tb = (int64_t)host::sm_count() * tper;
-        int64_t pb = (total + tb - 1) / tb;
-        pb = (pb + ids_per_stage - 1) / ids_per_stage * ids_per_stage;
-        int64_t nb = 0;
-        for (int s = 0; s < nseg; s++) {
-            a.blk_off[s] = (int)nb;
-            int64_t len = a.seg_off[s + 1] - a.seg_off[s];
-            nb += (len + pb - 1) / pb;
-        }
-        a.blk_off[nseg] = (int)nb;
-        if (nb == 0) return DS_OK;
-        fn<<<(unsigned)nb, MARK_THREADS, smem, (cudaStream_t)stream>>>(a, pb, 0);
-        return host::check_launch("ds_mark");
-    }
+    const int vec = (reinterpret_cast<uintptr_t>(idx) % 16 == 0) && ((a.seg_off[0] * isz) % 16 == 0);
     if (idx32)
         mark_kernel<int32_t><<<(unsigned)blocks, MARK_THREADS, 0, (cudaStream_t)stream>>>(
-            a, per_block, vec, use_cache);
+            a, per_block, vec, 1);
     else
         mark_kernel<int64_t><<<(unsigned)blocks, MARK_THREADS, 0, (cudaStream_t)stream>>>(
-            a, per_block, vec, use_cache);
+            a, per_block, vec, 1);
     return host::check_launch("ds_mark");
+}
+
+extern "C" int ds_mark_packed(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
+                              const void *lookups, const int64_t *seg_byte_off_host,
+                              const int64_t *seg_count_host, const int32_t *seg_width_host,
+                              const int32_t *seg_table_host, int nseg, uint32_t *flags,
+                              void *stream) {
+    return mark_packed_impl(words, word_off_host, rows_host, lookups, seg_byte_off_host,
+                            seg_count_host, seg_width_host, seg_table_host, nseg, flags, stream);
 }
 
 extern "C" int ds_mark(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,

@@ -18,6 +18,7 @@ import torch
 
 from . import _lib
 from .sharded import ShardedCheckpointer
+from .tracker import LookupStream
 
 
 class CheckpointPipeline:
@@ -58,23 +59,33 @@ class CheckpointPipeline:
         if self.keep:
             self.outputs.append((slot, n))
 
-    def submit(self, host_idx: torch.Tensor, seg_off, seg_tables) -> None:
-        """Queue one checkpoint interval whose lookups are in pinned host memory."""
+    def submit(self, host_idx, seg_off=None, seg_tables=None) -> None:
+        """Queue one checkpoint interval whose lookups are in pinned host
+        memory: a LookupStream (packed, mixed widths) or an index tensor split
+        by seg_off."""
         s = self.k & 1
-        n = host_idx.numel()
+        packed = isinstance(host_idx, LookupStream)
+        nbytes = host_idx.nbytes if packed else host_idx.numel() * host_idx.element_size()
+        if self.idx[s].numel() * self.idx[s].element_size() < nbytes:
+            raise ValueError("CheckpointPipeline: lookup stream larger than idx_capacity")
         # H2D: the slot's index buffer was last read by step k-2
         with torch.cuda.stream(self.h2d):
             if self.k >= 2:
                 self.h2d.wait_event(self.ev_done[s])
-            self.idx[s][:n].copy_(host_idx, non_blocking=True)
+            if packed:
+                dev_in = host_idx.to(self.ck.device, out=self.idx[s].view(torch.uint8))
+            else:
+                n = host_idx.numel()
+                self.idx[s][:n].copy_(host_idx, non_blocking=True)
+                dev_in = self.idx[s][:n]
             self.ev_in[s].record(self.h2d)
-        self.h2d_bytes += n * host_idx.element_size()
+        self.h2d_bytes += nbytes
         # compute: the slot's payload buffer must have left (D2H of step k-2)
         self.compute.wait_event(self.ev_in[s])
         if self.k >= 2:
             self.compute.wait_event(self.ev_out[s])
         self.ck.payload = self.payload[s]
-        self.ck.step(self.idx[s][:n], seg_off, seg_tables)
+        self.ck.step(dev_in, seg_off, seg_tables)
         self.nbytes_host[s:s + 1].copy_(self.ck.writer.sec_off[-1:], non_blocking=True)
         self.flags_host[s:s + 1].copy_(self.ck.writer.flags, non_blocking=True)
         self.ev_done[s].record(self.compute)

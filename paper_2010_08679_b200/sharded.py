@@ -21,16 +21,15 @@ import numpy as np
 import torch
 
 from . import _lib
-from .engine import DeviceTable, ShardWriter
+from .engine import DeviceTable, ShardWriter, adaptive_for
 from .payload import HEADER_SIZE, pack_header
-from .quant import AdaptiveConfig
-from .tracker import ModelTracker
+from .tracker import LookupStream, ModelTracker
 
 
 class ShardedCheckpointer:
     """One rank's part of a row-sharded incremental checkpoint."""
 
-    def __init__(self, tables: list, bitwidth: int | None, *, adaptive: AdaptiveConfig | None = None,
+    def __init__(self, tables: list, bitwidth: int | None, *, adaptive_overrides: dict | None = None,
                  rank: int = 0, world_size: int = 1, group=None, device=None,
                  scope: str = "interval"):
         self.tables = tables
@@ -43,6 +42,9 @@ class ShardedCheckpointer:
         self.tracker = ModelTracker({t.table_id: t.rows for t in tables}, device=self.device)
         # one rank writes whole sections (headers included); with several
         # ranks the runs are written bare and headers come from the counts
+        # ranges as the reference engine picks them (engine.py:112-115): the
+        # greedy search at 2/3/4 bits unless overridden, naive at 8
+        adaptive = adaptive_for(bitwidth, adaptive_overrides) if bitwidth is not None else None
         self.writer = ShardWriter(tables, bitwidth, adaptive=adaptive, device=self.device,
                                   write_headers=(world_size == 1))
         self.rec = self.writer.record_size(True)
@@ -55,48 +57,52 @@ class ShardedCheckpointer:
         self.capacity = sum(hdr + t.rows * self.rec for t in tables)
         self.payload = torch.empty(self.capacity + 16, dtype=torch.uint8, device=self.device)
         self._seg_cache = None
+        self._comm = torch.cuda.Stream(self.device) if world_size > 1 else None
 
     # -- the device-side step ---------------------------------------------------
 
-    def mark(self, idx: torch.Tensor, seg_off, seg_tables) -> None:
-        """K1 over a stream of lookups (int32 or int64 local row ids)."""
-        self.tracker.mark_batch(idx, seg_off, seg_tables)
+    def mark(self, idx, seg_off=None, seg_tables=None) -> None:
+        """K1 over a stream of lookups: a device LookupStream (packed, mixed
+        widths) or an int32/int64 tensor split by seg_off (local row ids)."""
+        if isinstance(idx, LookupStream):
+            self.tracker.mark_packed(idx)
+        else:
+            self.tracker.mark_batch(idx, seg_off, seg_tables)
 
     def checkpoint(self) -> None:
-        """K2 + count all_gather + K3, asynchronous on the current stream."""
+        """K2, then K3 overlapped with the count all_gather, asynchronous on the
+        current stream.  Only the host-side assembly needs the global counts, so
+        the collective runs on a side stream while the writer runs; the
+        current stream joins it before returning (step time includes it)."""
         fold = 1
         self.tracker.capture_into(self.ids, self.counts, fold=fold, scope=self.scope)
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(self.all_counts, self.counts, group=self.group)
-        self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
+            main = torch.cuda.current_stream(self.device)
+            self._comm.wait_stream(main)
+            with torch.cuda.stream(self._comm):
+                gather_counts(self.counts, self.world, self.group, out=self.all_counts)
+            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
+            main.wait_stream(self._comm)
+        else:
+            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
 
-    def step(self, idx: torch.Tensor, seg_off, seg_tables) -> None:
+    def step(self, idx, seg_off=None, seg_tables=None) -> None:
         self.mark(idx, seg_off, seg_tables)
         self.checkpoint()
 
     # -- host side ----------------------------------------------------------------
 
     def layout(self):
-        """(local payload bytes, per-table local counts, global offsets) after a sync.
-
-        Global layout of the shard payload: section t = header (24 B) + the
-        runs of ranks 0..N-1; this rank's run of table t starts at
-        run_off[t] (bytes from the payload start).
-        """
+        """(local payload bytes, per-table local counts, per-table totals,
+        section offsets, this rank's run offsets) after a sync; see shard_layout."""
         counts_all = self.all_counts.view(self.world, self.nt + 1).cpu().numpy() \
             if self.world > 1 else self.counts.view(1, self.nt + 1).cpu().numpy()
-        local = counts_all[self.rank, :self.nt]
-        per_table = counts_all[:, :self.nt].sum(axis=0)
-        sec_off = np.concatenate([[0], np.cumsum(HEADER_SIZE + per_table * self.rec)])
-        before = counts_all[:self.rank, :self.nt].sum(axis=0)
-        run_off = sec_off[:-1] + HEADER_SIZE + before * self.rec
+        per_table, sec_off, run_off = shard_layout(counts_all[:, :self.nt], self.rank, self.rec)
         nbytes = int(self.writer.sec_off[-1].item())
-        return nbytes, local, per_table, sec_off, run_off
+        return nbytes, counts_all[self.rank, :self.nt], per_table, sec_off, run_off
 
     def headers(self, per_table) -> list:
-        return [pack_header(t.table_id, int(n), t.dim, self.bitwidth, 1 if self.bitwidth else 0,
-                            False) for t, n in zip(self.tables, per_table)]
+        return section_headers(self.tables, per_table, self.bitwidth)
 
     def fetch(self, out: torch.Tensor | None = None, stream=None):
         """D2H of this rank's bytes into pinned memory; raises flagged errors."""
@@ -108,21 +114,71 @@ class ShardedCheckpointer:
         return out, nbytes
 
     def assemble(self, rank_bytes: list, per_table) -> bytes:
-        """Whole shard payload from every rank's fetched runs (host, rank order)."""
+        """Whole shard payload from every rank's (bytes, local counts) (host, rank order)."""
         if self.world == 1:
-            return bytes(rank_bytes[0])
-        parts = []
-        offs = [0] * self.world
-        counts = [None] * self.world
-        for g in range(self.world):
-            counts[g] = rank_bytes[g][1]
-        for t, hdr in enumerate(self.headers(per_table)):
-            parts.append(hdr)
-            for g in range(self.world):
-                n = int(counts[g][t]) * self.rec
-                parts.append(bytes(rank_bytes[g][0][offs[g]:offs[g] + n]))
-                offs[g] += n
-        return b"".join(parts)
+            return bytes(rank_bytes[0][0])
+        return assemble_shard(self.headers(per_table), [bytes(b[0]) for b in rank_bytes],
+                              np.stack([np.asarray(b[1]) for b in rank_bytes]), self.rec)
+
+
+# ---------------------------------------------------------------------------
+# host-side layout of a row-sharded shard payload (device independent)
+# ---------------------------------------------------------------------------
+
+def shard_layout(counts_all, rank: int, rec: int):
+    """Byte layout of one shard payload assembled from every rank's runs.
+
+    counts_all: (world, T) records per (rank, table).  Section t is one
+    24-byte header (payload.py:88-91) followed by the runs of ranks 0..N-1 in
+    rank order -- rows are sharded contiguously, so the runs concatenate to
+    the ascending row order of the reference section (payload.py:84-104).
+    Returns (per-table totals, section offsets [T+1], this rank's run offsets [T]).
+    """
+    counts_all = np.asarray(counts_all, dtype=np.int64)
+    per_table = counts_all.sum(axis=0)
+    sec_off = np.concatenate([[0], np.cumsum(HEADER_SIZE + per_table * rec)]).astype(np.int64)
+    before = counts_all[:rank].sum(axis=0)
+    run_off = sec_off[:-1] + HEADER_SIZE + before * rec
+    return per_table, sec_off, run_off
+
+
+def section_headers(tables, per_table, bitwidth, aux: bool = False) -> list:
+    """The 24-byte CNR1 headers of a row-sharded shard (global row counts)."""
+    return [pack_header(t.table_id, int(n), t.dim, bitwidth, 1 if bitwidth else 0, aux)
+            for t, n in zip(tables, per_table)]
+
+
+def assemble_shard(headers: list, runs: list, counts_all, rec: int) -> bytes:
+    """Shard payload from the headers and each rank's concatenated runs."""
+    counts_all = np.asarray(counts_all, dtype=np.int64)
+    world, nt = counts_all.shape
+    parts, offs = [], [0] * world
+    for t in range(nt):
+        parts.append(headers[t])
+        for g in range(world):
+            n = int(counts_all[g, t]) * rec
+            parts.append(runs[g][offs[g]:offs[g] + n])
+            offs[g] += n
+    for g in range(world):
+        if offs[g] != len(runs[g]):
+            raise ValueError(f"rank {g}: run bytes {len(runs[g])} != counted {offs[g]}")
+    return b"".join(parts)
+
+
+def gather_counts(counts: torch.Tensor, world: int, group=None,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """all_gather of every rank's int64 per-table counts (the only collective;
+    NCCL on GPUs, gloo in the CPU tests)."""
+    import torch.distributed as dist
+    if out is None:
+        out = torch.empty(world * counts.numel(), dtype=counts.dtype, device=counts.device)
+    if counts.is_cuda:
+        dist.all_gather_into_tensor(out, counts, group=group)
+    else:
+        parts = [torch.empty_like(counts) for _ in range(world)]
+        dist.all_gather(parts, counts, group=group)
+        out.copy_(torch.cat(parts))
+    return out
 
 
 def shard_rows(rows: int, world: int, rank: int) -> tuple:

@@ -267,6 +267,31 @@ class ModelTracker:
                                  tab_c.ctypes.data_as(ctypes.c_void_p), s1 - s0,
                                  self._flags.data_ptr(), stream), "mark_batch")
 
+    def mark_packed(self, stream: "LookupStream") -> None:
+        """K1 over a packed mixed-width lookup stream already on this device
+        (LookupStream.to); one launch per 64 segments."""
+        L = _lib.lib()
+        if stream.buf.device != self.device:
+            raise ValueError("mark_packed: move the stream to the tracker's device first")
+        pos = {tid: k for k, tid in enumerate(self._tids)}
+        tabs = np.array([pos[int(t)] for t in stream.seg_tables], dtype=np.int32)
+        for s0 in range(0, len(tabs), _lib.MAX_TABLES):
+            s1 = min(len(tabs), s0 + _lib.MAX_TABLES)
+            uniq = sorted(set(tabs[s0:s1].tolist()))
+            remap = {t: k for k, t in enumerate(uniq)}
+            wo_c = np.array([self._word_off[t] for t in uniq], dtype=np.int64)
+            rows_c = np.array([self._rows[self._tids[t]] for t in uniq], dtype=np.int64)
+            tab_c = np.array([remap[t] for t in tabs[s0:s1]], dtype=np.int32)
+            boff = np.ascontiguousarray(stream.seg_byte_off[s0:s1], dtype=np.int64)
+            cnt = np.ascontiguousarray(stream.seg_count[s0:s1], dtype=np.int64)
+            wid = np.ascontiguousarray(stream.seg_width[s0:s1], dtype=np.int32)
+            vp = ctypes.c_void_p
+            _lib.check(L.ds_mark_packed(
+                self._ibuf.data_ptr(), wo_c.ctypes.data_as(vp), rows_c.ctypes.data_as(vp),
+                stream.buf.data_ptr(), boff.ctypes.data_as(vp), cnt.ctypes.data_as(vp),
+                wid.ctypes.data_as(vp), tab_c.ctypes.data_as(vp), s1 - s0,
+                self._flags.data_ptr(), _lib.stream_handle()), "mark_packed")
+
     def capture_into(self, ids: torch.Tensor, counts: torch.Tensor, fold: int = 1,
                      scope: str = "interval") -> None:
         """K2 without any host synchronisation (the stall-window form).
@@ -359,3 +384,81 @@ class ModelTracker:
     def nbytes(self) -> int:
         return sum(b.nbytes for b in self._interval.values()) + sum(
             b.nbytes for b in self._baseline.values())
+
+
+# ---------------------------------------------------------------------------
+# packed lookup streams (ds_mark_packed)
+# ---------------------------------------------------------------------------
+
+def lookup_width(rows: int) -> int:
+    """Narrowest id width (bytes) for a table of `rows` rows: u8, u16, i32, i64."""
+    if rows <= 1 << 8:
+        return 1
+    if rows <= 1 << 16:
+        return 2
+    if rows <= 1 << 31:
+        return 4
+    return 8
+
+
+_WIDTH_DTYPE = {1: np.uint8, 2: np.uint16, 4: np.int32, 8: np.int64}
+
+
+class LookupStream:
+    """One interval's (or batch's) lookups of several tables, packed at the
+    narrowest width per table into one 16-byte-aligned byte buffer.
+
+    This is the wire format of K1's input: a data loader fills it on the host
+    (pinned), one H2D copy moves it, and ModelTracker.mark_packed consumes it.
+    Segment s = seg_count[s] ids of seg_width[s] bytes at seg_byte_off[s],
+    all of table seg_tables[s].
+    """
+
+    def __init__(self, buf: torch.Tensor, seg_byte_off, seg_count, seg_width, seg_tables):
+        self.buf = buf
+        self.seg_byte_off = np.asarray(seg_byte_off, dtype=np.int64)
+        self.seg_count = np.asarray(seg_count, dtype=np.int64)
+        self.seg_width = np.asarray(seg_width, dtype=np.int32)
+        self.seg_tables = np.asarray(seg_tables, dtype=np.int64)
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes of the stream (what one H2D copy moves)."""
+        return int(self.buf.numel())
+
+    @staticmethod
+    def layout(table_rows: dict, counts: dict):
+        """(byte offsets, counts, widths, table ids, total bytes) for {tid: count}."""
+        tids = list(counts)
+        boff, cnt, wid = [], [], []
+        off = 0
+        for t in tids:
+            w = lookup_width(int(table_rows[t]))
+            boff.append(off)
+            cnt.append(int(counts[t]))
+            wid.append(w)
+            off += (int(counts[t]) * w + 15) // 16 * 16
+        return boff, cnt, wid, tids, off
+
+    @classmethod
+    def pack(cls, lookups: dict, table_rows: dict, pin: bool = True) -> "LookupStream":
+        """Host-side packing of {table_id: integer ids} (ids are cast to the
+        table's width; out-of-range ids must already have been rejected by
+        the caller for widths 1 and 2, where they would wrap)."""
+        boff, cnt, wid, tids, total = cls.layout(table_rows, {t: len(v) for t, v in lookups.items()})
+        buf = torch.empty(max(16, total), dtype=torch.uint8, pin_memory=pin)
+        host = buf.numpy()
+        for t, o, n, w in zip(tids, boff, cnt, wid):
+            a = np.asarray(lookups[t])
+            if w <= 2 and a.size and (a.min() < 0 or a.max() >= table_rows[t]):
+                raise BoundsError(f"table {t}: row index out of range for a {8 * w}-bit stream")
+            host[o:o + n * w].view(_WIDTH_DTYPE[w])[:] = a
+        return cls(buf, boff, cnt, wid, tids)
+
+    def to(self, device, out: torch.Tensor | None = None, non_blocking: bool = True) -> "LookupStream":
+        """The same stream in device memory (one copy; `out` reuses a buffer)."""
+        if out is None:
+            out = torch.empty(self.buf.numel(), dtype=torch.uint8, device=device)
+        out[:self.buf.numel()].copy_(self.buf, non_blocking=non_blocking)
+        return LookupStream(out[:self.buf.numel()], self.seg_byte_off, self.seg_count,
+                            self.seg_width, self.seg_tables)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # quick GPU check: gpu tests + one bench line (+ optional ncu of the named kernels)
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python bench.py --no-cpu > gpurun_out/bq.json 2> gpurun_out/bq.err; echo "bench rc=$?"
 python - <<'P'
 import json

@@ -247,6 +247,47 @@ def test_mark_batch_multi_table(ds, O):
         assert np.array_equal(view.interval_rows[t], np.unique(idx[k]))
 
 
+@pytest.mark.parametrize("dtype", (torch.int32, torch.int64))
+def test_mark_batch_table_kinds_and_bounds(ds, dtype):
+    """Every per-table K1 form (shared byte map <= 16352 rows, shared bit
+    window <= 65536 rows, cache + RED above), boundary sizes, Zipf-like
+    repeats, ragged segment tails; out-of-range ids raise BoundsError at the
+    next sync and never leak a bit (the byte map's dummy byte at `rows`)."""
+    rng = np.random.default_rng(11)
+    sizes = [1, 31, 32, 33, 1000, 16351, 16352, 16353, 65535, 65536, 65537, 300_001]
+    rows = {t: r for t, r in enumerate(sizes)}
+    tr = ds.ModelTracker(rows)
+
+    def batch(bad=False):
+        idx, seg = [], [0]
+        for t, r in rows.items():
+            n = int(rng.integers(1, 40_000))
+            hot = rng.integers(0, r, 8)
+            a = np.where(rng.random(n) < 0.7, hot[rng.integers(0, 8, n)], rng.integers(0, r, n))
+            if bad and t % 3 == 0:
+                a[int(rng.integers(0, n))] = r if t % 2 == 0 else -1
+            idx.append(a)
+            seg.append(seg[-1] + a.size)
+        return idx, seg
+
+    idx, seg = batch()
+    tr.mark_batch(torch.from_numpy(np.concatenate(idx)).to(dtype).cuda(), np.array(seg),
+                  np.array(list(rows)))
+    view = tr.capture()
+    for k, t in enumerate(rows):
+        assert np.array_equal(view.interval_rows[t], np.unique(idx[k])), t
+    tr.reset_interval()
+    idx, seg = batch(bad=True)
+    tr.mark_batch(torch.from_numpy(np.concatenate(idx)).to(dtype).cuda(), np.array(seg),
+                  np.array(list(rows)))
+    with pytest.raises(ds.BoundsError):
+        tr.capture()
+    view = tr.capture()  # the valid ids of the batch are marked, nothing else
+    for k, (t, r) in enumerate(rows.items()):
+        good = idx[k][(idx[k] >= 0) & (idx[k] < r)]
+        assert np.array_equal(view.interval_rows[t], np.unique(good)), t
+
+
 # --- writer ------------------------------------------------------------------------
 
 class _Snap:
@@ -407,3 +448,39 @@ def test_restore_errors(ds, O):
         ds.restore_chain([("incremental", [blob])], {0: (4, 6)})
     with pytest.raises(ds.FormatError):
         ds.restore_chain([("incremental", [blob + b"\x01"])], shapes)
+
+
+# --- packed lookup streams (ds_mark_packed) ---------------------------------------
+
+def test_mark_packed_mixed_widths(ds):
+    """u8 / u16 / i32 segments of one packed stream, every table kind, Zipf
+    repeats and ragged lengths: the interval sets equal the unique ids."""
+    rng = np.random.default_rng(21)
+    rows = {0: 1, 1: 200, 2: 256, 3: 257, 4: 16352, 5: 40_000, 6: 65_536, 7: 65_537, 8: 2_000_000}
+    look = {}
+    for t, r in rows.items():
+        n = int(rng.integers(0, 30_000))
+        hot = rng.integers(0, r, 4)
+        look[t] = np.where(rng.random(n) < 0.6, hot[rng.integers(0, 4, n)], rng.integers(0, r, n))
+    st = ds.LookupStream.pack(look, rows)
+    assert [ds.lookup_width(r) for r in rows.values()] == [1, 1, 1, 2, 2, 2, 2, 4, 4]
+    assert st.seg_width.tolist() == [1, 1, 1, 2, 2, 2, 2, 4, 4]
+    tr = ds.ModelTracker(rows)
+    tr.mark_packed(st.to(tr.device))
+    view = tr.capture()
+    for t in rows:
+        assert np.array_equal(view.interval_rows[t], np.unique(look[t])), t
+
+
+def test_mark_packed_bounds(ds):
+    rows = {0: 100, 1: 70_000}
+    with pytest.raises(ds.BoundsError):  # would wrap at 8 bits: rejected on the host
+        ds.LookupStream.pack({0: np.array([5, 100])}, rows)
+    tr = ds.ModelTracker(rows)
+    st = ds.LookupStream.pack({0: np.array([5, 99]), 1: np.array([1, 70_000, -3, 69_999])}, rows)
+    tr.mark_packed(st.to(tr.device))
+    with pytest.raises(ds.BoundsError):  # i32 segment: flagged by the kernel
+        tr.capture()
+    view = tr.capture()
+    assert view.interval_rows[0].tolist() == [5, 99]
+    assert view.interval_rows[1].tolist() == [1, 69_999]
