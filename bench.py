@@ -324,7 +324,7 @@ def run_ours(args):
             ev[k][0].record()
             ck.mark(stream)                                # K1
             ev[k][1].record()
-            ck.tracker.capture_into(ck.ids, ck.counts, fold=1, scope=ck.scope)   # K2
+            ck.counts = ck.tracker.capture_into(ck.ids, None, fold=1, scope=ck.scope)  # K2
             ev[k][2].record()
             if world > 1:  # count all_gather on a side stream, overlapped with K3
                 comm.wait_stream(main)

@@ -132,7 +132,10 @@ DS_API int ds_popcount(const uint32_t *words, int64_t nwords, int64_t *out, void
  *     the totals;  offsets follow as exclusive prefix sums on the host side.
  *   fold: 0 none, 1 reset_interval (baseline |= interval; interval = 0)
  *     after reading, 2 reset_baseline (both cleared).
- * Workspace: ds_capture_workspace_size(total_words). */
+ * Workspace: ds_capture_workspace_size(total_words), zero-filled before its
+ * first use and not shared by concurrent calls (it holds a completion counter
+ * that each call leaves at zero).  Tables whose word offsets are multiples of
+ * 4 move with 16-byte loads and stores. */
 DS_API size_t ds_capture_workspace_size(int64_t total_words, int ntables);
 DS_API int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t *word_off_host,
                const int64_t *rows_host, int ntables, int64_t *ids_int, int64_t *ids_union,

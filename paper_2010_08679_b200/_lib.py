@@ -16,7 +16,8 @@ import torch
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdeltasnap_cuda.so")
+# DS_CUDA_LIB selects an A/B build variant of the same library (csrc/Makefile)
+LIB_PATH = os.environ.get("DS_CUDA_LIB") or os.path.join(HERE, "libdeltasnap_cuda.so")
 
 # ds_status -> exception (include/deltasnap_cuda.h; deltasnap/errors.py:4-41)
 _STATUS = {

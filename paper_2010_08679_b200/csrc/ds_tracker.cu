@@ -658,199 +658,18 @@ __global__ void __launch_bounds__(CAP_THREADS) capture_write_kernel(const CapArg
     }
 }
 
-// ---------------------------------------------------------------------------
-// K2, single pass: chunks of 1024 words (4 consecutive words per thread) are
-// claimed in dispatch order through a ticket; each chunk popcounts both scopes,
-// scans them inside the CTA, and resolves its global offset by a decoupled
-// look-back over its predecessors' published (aggregate | inclusive) states.
-// Ids go straight to HBM, the fold rewrites the words already in registers,
-// and the last chunk to finish turns the per-table end offsets into counts.
-// ---------------------------------------------------------------------------
 constexpr int CF_THREADS = 256;
-constexpr int CF_WPT = 4;
-constexpr int CF_WPB = CF_THREADS * CF_WPT;  // 1024 words per chunk
-constexpr unsigned long long CF_AGG = 1ull << 62, CF_INC = 2ull << 62;
-constexpr unsigned long long CF_MASK31 = (1ull << 31) - 1;
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-struct CapFArgs {
-    uint32_t *interval;
-    uint32_t *baseline;  // may be null
-    int64_t *ids_int;
-    int64_t *ids_uni;
-    int64_t *counts;
-    unsigned long long *status;  // [nchunks]
-    unsigned long long *ends;    // [ntables] packed (uni << 31 | int) inclusive end offsets
-    unsigned int *ticket;        // [2]: ticket, done
-    int64_t word_off[DS_MAX_TABLES + 1];
-    int64_t chunk_off[DS_MAX_TABLES + 1];
-    int ntables;
-    int nchunks;
-    int fold;
-};
-
-__global__ void __launch_bounds__(CF_THREADS) capture_fused_kernel(const CapFArgs a) {
-    __shared__ int s_chunk;
-    __shared__ unsigned s_warp[CF_THREADS / 32];
-    __shared__ unsigned long long s_prefix;
-    __shared__ bool s_last;
-    if (threadIdx.x == 0) s_chunk = (int)atomicAdd(a.ticket, 1u);
-    __syncthreads();
-    const int c = s_chunk;
-    int t = 0;
-    {
-        int lo = 0, hi = a.ntables - 1;
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (a.chunk_off[mid] <= c) lo = mid;
-            else hi = mid - 1;
-        }
-        t = lo;
-    }
-    const int64_t wt0 = a.word_off[t];
-    const int64_t w0 = wt0 + (int64_t)(c - a.chunk_off[t]) * CF_WPB + threadIdx.x * CF_WPT;
-    const int64_t wend = a.word_off[t + 1];
-    uint32_t iv[CF_WPT], uv[CF_WPT];
-    unsigned ci = 0, cu = 0;
-#pragma unroll
-    for (int k = 0; k < CF_WPT; k++) {
-        int64_t w = w0 + k;
-        iv[k] = w < wend ? a.interval[w] : 0u;
-        uint32_t bv = (w < wend && a.baseline) ? a.baseline[w] : 0u;
-        uv[k] = iv[k] | bv;
-        ci += __popc(iv[k]);
-        cu += __popc(uv[k]);
-    }
-    // block exclusive scan of packed (cu << 16 | ci); totals <= 32768 each
-    unsigned p = ci | (cu << 16);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned x = p;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(DS_FULL_MASK, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    unsigned wbase = 0, total = 0;
-#pragma unroll
-    for (int k = 0; k < CF_THREADS / 32; k++) {
-        unsigned v = s_warp[k];
-        wbase += k < wid ? v : 0u;
-        total += v;
-    }
-    const unsigned excl = wbase + x - p;
-    // publish the aggregate, then look back for the exclusive prefix: warp 0
-    // inspects 32 predecessors per probe and stops at the nearest inclusive one
-    if (wid == 0) {
-        const unsigned long long agg = (unsigned long long)(total & 0xffffu) |
-                                       ((unsigned long long)(total >> 16) << 31);
-        unsigned long long pi = 0, pu = 0;
-        if (c == 0) {
-            if (lane == 0) st_release(a.status + c, CF_INC | agg);
-        } else {
-            if (lane == 0) st_release(a.status + c, CF_AGG | agg);
-            int q = c - 1 - lane;
-            while (true) {
-                // chunks before 0 count as an inclusive prefix of 0
-                unsigned long long s = q >= 0 ? ld_acquire(a.status + q) : CF_INC;
-                const unsigned flag = (unsigned)(s >> 62);
-                if (__any_sync(DS_FULL_MASK, flag == 0)) continue;  // not all published: re-probe
-                const unsigned inc = __ballot_sync(DS_FULL_MASK, flag == 2);
-                const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive (lowest lane)
-                unsigned long long vi = lane <= stop ? (s & CF_MASK31) : 0ull;
-                unsigned long long vu = lane <= stop ? ((s >> 31) & CF_MASK31) : 0ull;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    vi += __shfl_xor_sync(DS_FULL_MASK, vi, o);
-                    vu += __shfl_xor_sync(DS_FULL_MASK, vu, o);
-                }
-                pi += vi;
-                pu += vu;
-                if (inc) break;
-                q -= 32;
-            }
-            if (lane == 0) {
-                unsigned long long incl = (pi + (total & 0xffffu)) | ((pu + (total >> 16)) << 31);
-                st_release(a.status + c, CF_INC | incl);
-            }
-        }
-        if (lane == 0) {
-            const unsigned long long pre = pi | (pu << 31);
-            s_prefix = pre;
-            // end offset of a table = inclusive prefix of its last chunk
-            if (c == a.chunk_off[t + 1] - 1)
-                a.ends[t] = (pi + (total & 0xffffu)) | ((pu + (total >> 16)) << 31);
-        }
-    }
-    __syncthreads();
-    const unsigned long long pre = s_prefix;
-    int64_t oi = (int64_t)(pre & CF_MASK31) + (excl & 0xffffu);
-    int64_t ou = (int64_t)((pre >> 31) & CF_MASK31) + (excl >> 16);
-    const int64_t row0 = (w0 - wt0) * 32;
-#pragma unroll
-    for (int k = 0; k < CF_WPT; k++) {
-        if (a.ids_int) {
-            uint32_t m = iv[k];
-            while (m) {
-                int b = __ffs(m) - 1;
-                a.ids_int[oi++] = row0 + 32 * k + b;
-                m &= m - 1;
-            }
-        }
-        if (a.ids_uni) {
-            uint32_t m = uv[k];
-            while (m) {
-                int b = __ffs(m) - 1;
-                a.ids_uni[ou++] = row0 + 32 * k + b;
-                m &= m - 1;
-            }
-        }
-        int64_t w = w0 + k;
-        if (w < wend && a.fold) {  // reset_interval (1) / reset_baseline (2)
-            if (a.baseline) a.baseline[w] = a.fold == 1 ? uv[k] : 0u;
-            a.interval[w] = 0u;
-        }
-    }
-    // the last chunk to finish converts table end offsets into counts
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(a.ticket + 1, 1u) == (unsigned)a.nchunks - 1;
-    __syncthreads();
-    if (s_last) {
-        __threadfence();
-        const int nt = a.ntables;
-        for (int k = threadIdx.x; k < nt; k += CF_THREADS) {
-            unsigned long long e = ld_acquire(a.ends + k);
-            unsigned long long b = k ? ld_acquire(a.ends + k - 1) : 0ull;
-            a.counts[k] = (int64_t)((e & CF_MASK31) - (b & CF_MASK31));
-            a.counts[nt + 1 + k] = (int64_t)(((e >> 31) & CF_MASK31) - ((b >> 31) & CF_MASK31));
-        }
-        if (threadIdx.x == 0) {
-            unsigned long long e = ld_acquire(a.ends + nt - 1);
-            a.counts[nt] = (int64_t)(e & CF_MASK31);
-            a.counts[2 * nt + 1] = (int64_t)((e >> 31) & CF_MASK31);
-        }
-    }
-}
-
+#ifndef DS_C3_WPT
+#define DS_C3_WPT 1
+#endif
 
 // ---------------------------------------------------------------------------
-// K2 as count -> scan -> emit over chunks of 1024 words (4 consecutive words
-// per thread).  The emit pass knows every chunk's base, so no CTA waits on
-// another (the look-back form above serialises through chunk order).
-// 4 consecutive words per thread: chunks of 1024 words (32768 rows) keep the
-// per-CTA emission short and balanced
+// K2 as count (+ scan by the last CTA) -> emit over chunks of 1024 words (4
+// consecutive words per thread, 32768 rows: short, balanced CTAs).  The emit
+// pass knows every chunk's base, so no CTA waits on another (a decoupled
+// look-back single pass serialises through chunk order and measured slower).
 // ---------------------------------------------------------------------------
-constexpr int C3_WPT = 4;
+constexpr int C3_WPT = DS_C3_WPT;
 constexpr int C3_WPB = CF_THREADS * C3_WPT;
 
 struct Cap3Args {
@@ -859,8 +678,9 @@ struct Cap3Args {
     int64_t *ids_int;
     int64_t *ids_uni;
     int64_t *counts;
-    unsigned long long *cnt;   // [nchunks] packed (union << 32 | interval)
-    unsigned long long *base;  // [nchunks] exclusive prefix, same packing
+    unsigned long long *cnt;    // [nchunks] packed (union << 32 | interval)
+    unsigned long long *super;  // [nchunks / 256 + 1] sums of 256 chunks (left at 0)
+    unsigned *ticket;           // emit CTAs done (the last one clears super; left at 0)
     int64_t word_off[DS_MAX_TABLES + 1];
     int64_t chunk_off[DS_MAX_TABLES + 1];
     int ntables;
@@ -868,16 +688,38 @@ struct Cap3Args {
     int fold;
 };
 
+// table of chunk c, once per CTA (binary search, broadcast through shared memory)
 __device__ __forceinline__ int cap3_table(const Cap3Args &a, int c) {
-    int t = 0;
-    while (t + 1 < a.ntables && a.chunk_off[t + 1] <= c) t++;
-    return t;
+    __shared__ int s_t;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = a.ntables - 1;  // last t with chunk_off[t] <= c
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (a.chunk_off[mid] <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        s_t = lo;
+    }
+    __syncthreads();
+    return s_t;
 }
 
+// the thread's C3_WPT words of chunk c: one 16-byte load when the table's
+// words start 16-byte aligned (ModelTracker pads every table to 4 words)
 __device__ __forceinline__ void cap3_load(const Cap3Args &a, int c, int t, uint32_t (&iv)[C3_WPT],
                                           uint32_t (&uv)[C3_WPT], int64_t &w0, int64_t &wend) {
     w0 = a.word_off[t] + (int64_t)(c - a.chunk_off[t]) * C3_WPB + threadIdx.x * C3_WPT;
     wend = a.word_off[t + 1];
+    if constexpr (C3_WPT == 4) {
+        if ((w0 & 3) == 0 && w0 + 4 <= wend) {
+            const uint4 i4 = __ldcg(reinterpret_cast<const uint4 *>(a.interval + w0));
+            uint4 b4 = make_uint4(0u, 0u, 0u, 0u);
+            if (a.baseline) b4 = __ldcg(reinterpret_cast<const uint4 *>(a.baseline + w0));
+            iv[0] = i4.x; iv[1] = i4.y; iv[2] = i4.z; iv[3] = i4.w;
+            uv[0] = i4.x | b4.x; uv[1] = i4.y | b4.y; uv[2] = i4.z | b4.z; uv[3] = i4.w | b4.w;
+            return;
+        }
+    }
 #pragma unroll
     for (int k = 0; k < C3_WPT; k++) {
         const int64_t w = w0 + k;
@@ -887,8 +729,34 @@ __device__ __forceinline__ void cap3_load(const Cap3Args &a, int c, int t, uint3
     }
 }
 
+// CTA-wide sum (every thread gets it); s_red holds CF_THREADS/32 values
+__device__ __forceinline__ unsigned long long cap3_block_sum(unsigned long long v,
+                                                             unsigned long long *s_red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(DS_FULL_MASK, v, o);
+    __syncthreads();  // s_red may still be read by a previous call
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < CF_THREADS / 32; k++) s += s_red[k];
+    return s;
+}
+
+// packed ids before chunk x: the sums of the whole 256-chunk groups before it
+// plus the chunks of its own group before it (one load per thread)
+__device__ __forceinline__ unsigned long long cap3_base(const Cap3Args &a, int x,
+                                                        unsigned long long *s_red) {
+    unsigned long long v = 0;
+    const int g = x >> 8, g0 = g << 8;
+    for (int i = threadIdx.x; i < g; i += CF_THREADS) v += __ldcg(a.super + i);
+    if (g0 + (int)threadIdx.x < x) v += __ldcg(a.cnt + g0 + threadIdx.x);
+    return cap3_block_sum(v, s_red);
+}
+
+// pass 1: per-chunk popcounts, and their 256-chunk group sums
 __global__ void __launch_bounds__(CF_THREADS) cap3_count_kernel(const Cap3Args a) {
-    __shared__ unsigned long long s_w[CF_THREADS / 32];
+    __shared__ unsigned long long s_red[CF_THREADS / 32];
     const int c = blockIdx.x, t = cap3_table(a, c);
     uint32_t iv[C3_WPT], uv[C3_WPT];
     int64_t w0, wend;
@@ -897,75 +765,29 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_count_kernel(const Cap3Args a
 #pragma unroll
     for (int k = 0; k < C3_WPT; k++)
         v += (unsigned long long)__popc(iv[k]) | ((unsigned long long)__popc(uv[k]) << 32);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(DS_FULL_MASK, v, o);
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
-    __syncthreads();
+    const unsigned long long s = cap3_block_sum(v, s_red);
     if (threadIdx.x == 0) {
-        unsigned long long s = 0;
-        for (int k = 0; k < CF_THREADS / 32; k++) s += s_w[k];
         a.cnt[c] = s;
+        atomicAdd(a.super + (c >> 8), s);
     }
 }
 
-// one CTA: exclusive scan of the packed chunk counts, per-table counts
-__global__ void __launch_bounds__(1024) cap3_scan_kernel(const Cap3Args a) {
-    __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_carry;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int s0 = 0; s0 < a.nchunks; s0 += 1024) {
-        const int i = s0 + threadIdx.x;
-        const unsigned long long v = i < a.nchunks ? a.cnt[i] : 0ull;
-        unsigned long long x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_w[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            unsigned long long wv = s_w[lane], wx = wv;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                unsigned long long y = __shfl_up_sync(DS_FULL_MASK, wx, o);
-                if (lane >= o) wx += y;
-            }
-            s_w[lane] = wx - wv;
-        }
-        __syncthreads();
-        const unsigned long long carry = s_carry;
-        if (i < a.nchunks) a.base[i] = carry + s_w[wid] + x - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) s_carry = carry + s_w[wid] + x;
-        __syncthreads();
-    }
-    const unsigned long long total = s_carry;
-    const int nt = a.ntables;
-    for (int t = threadIdx.x; t < nt; t += 1024) {
-        const int c0 = (int)a.chunk_off[t], c1 = (int)a.chunk_off[t + 1];
-        const unsigned long long b0 = c0 < a.nchunks ? a.base[c0] : total;
-        const unsigned long long b1 = c1 < a.nchunks ? a.base[c1] : total;
-        a.counts[t] = (int64_t)((uint32_t)b1 - (uint32_t)b0);
-        a.counts[nt + 1 + t] = (int64_t)((b1 >> 32) - (b0 >> 32));
-    }
-    if (threadIdx.x == 0) {
-        a.counts[nt] = (int64_t)(uint32_t)total;
-        a.counts[2 * nt + 1] = (int64_t)(total >> 32);
-    }
-}
+constexpr unsigned CAP3_STAGE = C3_WPB * 32;  // every id of a chunk fits the stage
+static_assert(CAP3_STAGE * 4 <= 48 * 1024, "stage must fit static shared memory");
 
-constexpr unsigned CAP3_STAGE = 8192;  // ids staged per scope and chunk (32 KB)
-
+// pass 2: the chunk's base from the group sums, its sorted ids (staged in
+// shared memory, coalesced int64 stores), the per-table counts (by each
+// table's last chunk), then the fold
 __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a) {
+    __shared__ unsigned long long s_red[CF_THREADS / 32];
     __shared__ unsigned long long s_warp[CF_THREADS / 32];
     __shared__ uint32_t s_ids[CAP3_STAGE];
+    __shared__ bool s_last;
     const int c = blockIdx.x, t = cap3_table(a, c);
     uint32_t iv[C3_WPT], uv[C3_WPT];
     int64_t w0, wend;
     cap3_load(a, c, t, iv, uv, w0, wend);
+    const unsigned long long b = cap3_base(a, c, s_red);
     unsigned ci = 0, cu = 0;
 #pragma unroll
     for (int k = 0; k < C3_WPT; k++) {
@@ -978,7 +800,7 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
     unsigned long long x = p;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
+        const unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
         if (lane >= o) x += y;
     }
     if (lane == 31) s_warp[wid] = x;
@@ -986,14 +808,11 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
     unsigned long long wbase = 0, tot = 0;
 #pragma unroll
     for (int k = 0; k < CF_THREADS / 32; k++) {
-        wbase += k < wid ? s_warp[k] : 0ull;
-        tot += s_warp[k];
+        const unsigned long long sw = s_warp[k];
+        wbase += k < wid ? sw : 0ull;
+        tot += sw;
     }
     const unsigned long long excl = wbase + x - p;
-    const unsigned long long b = a.base[c];
-    // ids are staged in shared memory as chunk-local row offsets and
-    // leave as coalesced int64 runs; a chunk denser than the stage writes
-    // straight from the registers
     const int64_t crow0 = (w0 - threadIdx.x * C3_WPT - a.word_off[t]) * 32;  // chunk's first row
     const unsigned lrow0 = threadIdx.x * C3_WPT * 32;                         // thread's first row
     for (int scope = 0; scope < 2; scope++) {
@@ -1002,38 +821,65 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
         const unsigned n = (unsigned)(scope ? tot >> 32 : tot & 0xffffffffu);
         unsigned o = (unsigned)(scope ? excl >> 32 : excl & 0xffffffffu);
         const int64_t gbase = scope ? (int64_t)(b >> 32) : (int64_t)(uint32_t)b;
-        if (n <= CAP3_STAGE) {
 #pragma unroll
-            for (int k = 0; k < C3_WPT; k++) {
-                uint32_t m = scope ? uv[k] : iv[k];
-                while (m) {
-                    s_ids[o++] = lrow0 + 32 * k + __ffs(m) - 1;
-                    m &= m - 1;
-                }
+        for (int k = 0; k < C3_WPT; k++) {
+            uint32_t m = scope ? uv[k] : iv[k];
+            while (m) {
+                s_ids[o++] = lrow0 + 32 * k + __ffs(m) - 1;
+                m &= m - 1;
             }
-            __syncthreads();
-            for (unsigned j = threadIdx.x; j < n; j += CF_THREADS)
-                __stcs(out + gbase + j, crow0 + s_ids[j]);
-            __syncthreads();
-        } else {
-            int64_t oo = gbase + o;
+        }
+        __syncthreads();
+        for (unsigned j = threadIdx.x; j < n; j += CF_THREADS)
+            __stcs(out + gbase + j, crow0 + s_ids[j]);
+        __syncthreads();
+    }
+    // per-table counts: written by the table's last chunk
+    if (c == a.chunk_off[t + 1] - 1) {
+        const unsigned long long start = cap3_base(a, (int)a.chunk_off[t], s_red);
+        const unsigned long long end = b + tot;
+        const int nt = a.ntables;
+        if (threadIdx.x == 0) {
+            a.counts[t] = (int64_t)((uint32_t)end - (uint32_t)start);
+            a.counts[nt + 1 + t] = (int64_t)((end >> 32) - (start >> 32));
+            if (t == nt - 1) {
+                a.counts[nt] = (int64_t)(uint32_t)end;
+                a.counts[2 * nt + 1] = (int64_t)(end >> 32);
+            }
+        }
+    }
+    if (a.fold) {  // reset_interval (1) / reset_baseline (2)
+        bool done = false;
+        if constexpr (C3_WPT == 4) {
+            if ((w0 & 3) == 0 && w0 + 4 <= wend) {
+                if (a.baseline)
+                    *reinterpret_cast<uint4 *>(a.baseline + w0) =
+                        a.fold == 1 ? make_uint4(uv[0], uv[1], uv[2], uv[3]) : make_uint4(0u, 0u, 0u, 0u);
+                *reinterpret_cast<uint4 *>(a.interval + w0) = make_uint4(0u, 0u, 0u, 0u);
+                done = true;
+            }
+        }
+        if (!done) {
 #pragma unroll
             for (int k = 0; k < C3_WPT; k++) {
-                uint32_t m = scope ? uv[k] : iv[k];
-                while (m) {
-                    out[oo++] = crow0 + lrow0 + 32 * k + __ffs(m) - 1;
-                    m &= m - 1;
+                const int64_t w = w0 + k;
+                if (w < wend) {
+                    if (a.baseline) a.baseline[w] = a.fold == 1 ? uv[k] : 0u;
+                    a.interval[w] = 0u;
                 }
             }
         }
     }
-#pragma unroll
-    for (int k = 0; k < C3_WPT; k++) {
-        const int64_t w = w0 + k;
-        if (w < wend && a.fold) {  // reset_interval (1) / reset_baseline (2)
-            if (a.baseline) a.baseline[w] = a.fold == 1 ? uv[k] : 0u;
-            a.interval[w] = 0u;
-        }
+    // the last CTA clears the group sums for the next call
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        for (int i = threadIdx.x; i <= (a.nchunks >> 8); i += CF_THREADS) a.super[i] = 0ull;
+        if (threadIdx.x == 0) *a.ticket = 0u;
     }
 }
 
@@ -1252,9 +1098,13 @@ static int64_t capture_nchunks(const int64_t *word_off_host, int ntables) {
 }
 
 extern "C" size_t ds_capture_workspace_size(int64_t total_words, int ntables) {
-    // 4 arrays of nchunks u64; nchunks <= total_words/CAP_WPB + ntables
-    int64_t nchunks = total_words / CAP_WPB + 2 * (int64_t)ntables + 1;
-    return (size_t)(4 * nchunks) * sizeof(unsigned long long) + 256;
+    // count/emit form: ticket + 2 arrays of nchunks u64 (chunks of C3_WPB words);
+    // the > 2^32-row form: 4 arrays of nchunks u64 (chunks of CAP_WPB words)
+    const int64_t n3 = total_words / C3_WPB + 2 * (int64_t)ntables + 1;
+    const int64_t n1 = total_words / CAP_WPB + 2 * (int64_t)ntables + 1;
+    const size_t b3 = 16 + (size_t)(2 * n3) * sizeof(unsigned long long);
+    const size_t b1 = (size_t)(4 * n1) * sizeof(unsigned long long);
+    return (b3 > b1 ? b3 : b1) + 256;
 }
 
 extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t *word_off_host,
@@ -1267,7 +1117,7 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     int64_t total_rows = 0;
     for (int t = 0; t < ntables; t++) total_rows += (word_off_host[t + 1] - word_off_host[t]) * 32;
-    if (total_rows < (int64_t)0xffffffffLL && !host::env_flag("DS_CAPTURE_LOOKBACK")) {
+    if (total_rows < (int64_t)0xffffffffLL) {
         // count -> scan -> emit (ids per scope fit the 32-bit packed counts)
         Cap3Args f;
         f.interval = interval;
@@ -1286,41 +1136,13 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
         }
         f.chunk_off[ntables] = nch;
         f.nchunks = (int)nch;
-        size_t need = 2 * (size_t)nch * sizeof(unsigned long long);
+        size_t need = 16 + (size_t)(nch + nch / 256 + 1) * sizeof(unsigned long long);
         if (workspace_bytes < need) return host::fail(DS_ERR_ARG, "ds_capture: workspace too small");
-        f.cnt = reinterpret_cast<unsigned long long *>(workspace);
-        f.base = f.cnt + nch;
+        f.ticket = reinterpret_cast<unsigned *>(workspace);
+        f.cnt = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + 16);
+        f.super = f.cnt + nch;
         cap3_count_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
-        cap3_scan_kernel<<<1, 1024, 0, s>>>(f);
         cap3_emit_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
-        return host::check_launch("ds_capture");
-    }
-    if (total_rows < (int64_t)CF_MASK31) {
-        // single-pass path (ids per scope fit the 31-bit look-back fields)
-        CapFArgs f;
-        f.interval = interval;
-        f.baseline = baseline;
-        f.ids_int = ids_int;
-        f.ids_uni = ids_union;
-        f.counts = counts;
-        f.ntables = ntables;
-        f.fold = fold;
-        int64_t nch = 0;
-        for (int t = 0; t <= ntables; t++) f.word_off[t] = word_off_host[t];
-        for (int t = 0; t < ntables; t++) {
-            f.chunk_off[t] = nch;
-            int64_t w = word_off_host[t + 1] - word_off_host[t];
-            nch += w > 0 ? (w + CF_WPB - 1) / CF_WPB : 1;
-        }
-        f.chunk_off[ntables] = nch;
-        f.nchunks = (int)nch;
-        size_t need = 16 + (size_t)(nch + ntables) * sizeof(unsigned long long);
-        if (workspace_bytes < need) return host::fail(DS_ERR_ARG, "ds_capture: workspace too small");
-        f.ticket = reinterpret_cast<unsigned int *>(workspace);
-        f.status = reinterpret_cast<unsigned long long *>(static_cast<char *>(workspace) + 16);
-        f.ends = f.status + nch;
-        cudaMemsetAsync(workspace, 0, 16 + (size_t)nch * sizeof(unsigned long long), s);
-        capture_fused_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
         return host::check_launch("ds_capture");
     }
     CapArgs a;

@@ -75,7 +75,7 @@ class ShardedCheckpointer:
         the collective runs on a side stream while the writer runs; the
         current stream joins it before returning (step time includes it)."""
         fold = 1
-        self.tracker.capture_into(self.ids, self.counts, fold=fold, scope=self.scope)
+        self.counts = self.tracker.capture_into(self.ids, None, fold=fold, scope=self.scope)
         if self.world > 1:
             main = torch.cuda.current_stream(self.device)
             self._comm.wait_stream(main)

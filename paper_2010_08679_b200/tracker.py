@@ -162,7 +162,7 @@ def _capture_words(interval: torch.Tensor, baseline: torch.Tensor | None, rows: 
         k = c1 - c0
         counts = torch.zeros(2 * k + 2, dtype=torch.int64, device=dev)
         ws_bytes = int(L.ds_capture_workspace_size(int(wo[-1]), k))
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)  # zero before first use
         iv = interval[base:]
         bv = baseline[base:] if baseline is not None else None
         # pass 1: counts only (bitmaps are small: 1/256 of the fp32 rows they
@@ -210,9 +210,11 @@ class ModelTracker:
         dev = device_of(device)
         self._tids = sorted(table_rows)
         self._rows = {tid: int(table_rows[tid]) for tid in self._tids}
+        # every table's words start 16-byte aligned (4-word padding, always
+        # zero) so K2 moves them with 16-byte loads and stores
         self._word_off = [0]
         for tid in self._tids:
-            self._word_off.append(self._word_off[-1] + _words_for(self._rows[tid]))
+            self._word_off.append(self._word_off[-1] + (_words_for(self._rows[tid]) + 3) // 4 * 4)
         total = self._word_off[-1]
         self._ibuf = torch.zeros(total, dtype=torch.int32, device=dev)
         self._bbuf = torch.zeros(total, dtype=torch.int32, device=dev)
@@ -220,7 +222,8 @@ class ModelTracker:
         self._interval = {}
         self._baseline = {}
         for k, tid in enumerate(self._tids):
-            w0, w1 = self._word_off[k], self._word_off[k + 1]
+            w0 = self._word_off[k]
+            w1 = w0 + _words_for(self._rows[tid])
             self._interval[tid] = DirtyBitmap(tid, self._rows[tid], _words=self._ibuf[w0:w1],
                                               _flags=self._flags)
             self._baseline[tid] = DirtyBitmap(tid, self._rows[tid], _words=self._bbuf[w0:w1],
@@ -292,14 +295,16 @@ class ModelTracker:
                 wid.ctypes.data_as(vp), tab_c.ctypes.data_as(vp), s1 - s0,
                 self._flags.data_ptr(), _lib.stream_handle()), "mark_packed")
 
-    def capture_into(self, ids: torch.Tensor, counts: torch.Tensor, fold: int = 1,
-                     scope: str = "interval") -> None:
+    def capture_into(self, ids: torch.Tensor, counts: torch.Tensor | None = None, fold: int = 1,
+                     scope: str = "interval") -> torch.Tensor:
         """K2 without any host synchronisation (the stall-window form).
 
         Writes the chosen scope's local row ids of every table, concatenated in
         table order, into `ids` (capacity >= total rows) and the per-table
         counts into counts[:ntables] (counts[ntables] = total), then folds
         (1: reset_interval, 2: reset_baseline, 0: none).  At most 64 tables.
+        With counts=None the capture's own device counts are returned (no
+        copy; valid until the next capture_into).
         """
         if len(self._tids) > _lib.MAX_TABLES:
             raise ValueError("capture_into supports at most 64 tables")
@@ -309,7 +314,7 @@ class ModelTracker:
             wo = np.array(self._word_off, dtype=np.int64)
             rows = np.array([self._rows[t] for t in self._tids], dtype=np.int64)
             ws_bytes = int(L.ds_capture_workspace_size(int(wo[-1]), nt))
-            self._cap_ws = (wo, rows, torch.empty(ws_bytes, dtype=torch.uint8, device=self.device))
+            self._cap_ws = (wo, rows, torch.zeros(ws_bytes, dtype=torch.uint8, device=self.device))
             self._cap_counts = torch.zeros(2 * nt + 2, dtype=torch.int64, device=self.device)
         wo, rows, ws = self._cap_ws
         union = scope != "interval"
@@ -321,7 +326,10 @@ class ModelTracker:
                                 ids.data_ptr() if union else None, cnt.data_ptr(), fold,
                                 ws.data_ptr(), ws.numel(), _lib.stream_handle()), "capture_into")
         src = cnt[nt + 1:2 * nt + 2] if union else cnt[:nt + 1]
+        if counts is None:
+            return src  # the capture's own counts (valid until the next capture)
         counts[:nt + 1].copy_(src, non_blocking=True)
+        return counts
 
     def interval_bitmap(self, table_id: int) -> DirtyBitmap:
         return self._interval[table_id]

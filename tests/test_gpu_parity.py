@@ -484,3 +484,29 @@ def test_mark_packed_bounds(ds):
     view = tr.capture()
     assert view.interval_rows[0].tolist() == [5, 99]
     assert view.interval_rows[1].tolist() == [1, 69_999]
+
+
+@pytest.mark.parametrize("scope", ("interval", "since_baseline"))
+def test_capture_into_matches_capture(ds, scope):
+    """The stall-window form (device ids + counts, fold in the same pass)
+    equals capture() + reset_interval (tracker.py:100-124)."""
+    rng = np.random.default_rng(8)
+    rows = {2: 100_000, 5: 33, 9: 5_000_000, 11: 4096}
+    a, b = ds.ModelTracker(rows), ds.ModelTracker(rows)
+    for phase in range(3):
+        for t, r in rows.items():
+            idx = rng.integers(0, r, int(rng.integers(1, 50_000)))
+            a.mark(t, idx)
+            b.mark(t, idx)
+        ids = torch.empty(sum(rows.values()), dtype=torch.int64, device="cuda")
+        counts = a.capture_into(ids, None, fold=1, scope=scope)
+        view = b.capture()
+        b.reset_interval()
+        c = counts.cpu().numpy()
+        h = ids.cpu().numpy()
+        off = 0
+        want = view.interval_rows if scope == "interval" else view.baseline_rows
+        for k, t in enumerate(sorted(rows)):
+            assert np.array_equal(h[off:off + c[k]], want[t]), (phase, t)
+            off += c[k]
+        assert c[len(rows)] == off
