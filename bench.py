@@ -37,11 +37,36 @@ sys.path.insert(0, ROOT)
 
 CRITEO_KAGGLE = [1460, 583, 10131227, 2202608, 305, 24, 12517, 633, 3, 93145, 5683, 8351593,
                  3194, 27, 14992, 5461306, 10, 5652, 2173, 4, 7046547, 18, 15, 286181, 105, 142572]
-DIM = 16
-BITWIDTH = 8
+# MLPerf DLRM Criteo-Terabyte cardinalities (capped at 40M rows), 187.8M rows
+CRITEO_TB = [39884406, 39043, 17289, 7420, 20263, 3, 7120, 1543, 63, 38532951, 2953546, 403346,
+             10, 2208, 11938, 155, 4, 976, 14, 39979771, 25641295, 39664984, 585935, 12972, 108, 36]
 BATCHES = 500
 BATCH = 2048
 ZIPF_S = 1.05
+
+# BASELINE.json configs as single-GPU workloads (per-rank shards; weak scaling)
+WORKLOADS = {
+    # configs[1]: the metric's headline config (the default)
+    "C2": dict(desc="C2: Criteo-Kaggle-shaped 26 tables x dim 16 fp32, 8-bit naive, checkpoint "
+                    "every 500 batches x 2048 Zipf(1.05) lookups/table",
+               cards=CRITEO_KAGGLE, dim=16, bitwidth=8, adaptive=False, lookups="zipf",
+               n_per_table=BATCHES * BATCH),
+    # the north-star target T, one GPU's shard of 1B x 128 over 8 GPUs:
+    # 125M rows, 4-bit incremental, ~26% of rows dirty per interval
+    "T": dict(desc="T (one of 8 GPU shards): 125M rows x dim 128 fp32 (64 GB), 4-bit naive "
+                   "incremental, 37.5M uniform lookups per interval (26% of rows dirty)",
+              cards=[125_000_000], dim=128, bitwidth=4, adaptive=False, lookups="uniform",
+              n_per_table=37_500_000),
+    "T-adaptive": dict(desc="T shard with the reference's 4-bit default ranges: adaptive greedy "
+                            "(bins 45, ratio 0.2)",
+                       cards=[125_000_000], dim=128, bitwidth=4, adaptive=True, lookups="uniform",
+                       n_per_table=37_500_000),
+    # configs[2], one of 8 GPU shards: Criteo-TB rows / 8, 4-bit adaptive greedy
+    "C3": dict(desc="C3 (one of 8 GPU shards): Criteo-TB-shaped 26 tables / 8 x dim 128 fp32, "
+                    "4-bit adaptive greedy (bins 45, ratio 0.2), 500 x 2048 Zipf lookups/table",
+               cards=[max(1, c // 8) for c in CRITEO_TB], dim=128, bitwidth=4, adaptive=True,
+               lookups="zipf", n_per_table=BATCHES * BATCH),
+}
 METRIC = "checkpointed GB/s of embedding rows (track+quantize+pack) at 1/2/4/8 B200 vs CPU ref"
 
 
@@ -54,25 +79,34 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--tables", type=int, default=len(CRITEO_KAGGLE),
+    p.add_argument("--tables", type=int, default=0,
                    help="use the first T tables (smoke/profiling only)")
+    p.add_argument("--workload", choices=sorted(WORKLOADS), default="C2",
+                   help="BASELINE.json config (C2 is the metric's headline config)")
     p.add_argument("--l2-fetch", type=int, default=64,
                    help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default)")
     return p.parse_args()
 
 
-def workload_desc(cards, n_lookups_per_table):
+def workload_of(args):
+    w = dict(WORKLOADS[args.workload])
+    if args.tables:
+        w["cards"] = w["cards"][:args.tables]
+    return w
+
+
+def workload_desc(w):
     return {
-        "workload": "C2: Criteo-Kaggle-shaped 26 tables x dim 16 fp32, 8-bit naive, "
-                    "checkpoint every 500 batches x 2048 Zipf(1.05) lookups/table",
-        "tables": len(cards), "rows_per_rank": int(sum(cards)), "dim": DIM,
-        "bitwidth": BITWIDTH, "batches_per_interval": BATCHES, "batch": BATCH,
-        "lookups_per_step_per_rank": int(n_lookups_per_table * len(cards)),
+        "workload": w["desc"], "name": [k for k, v in WORKLOADS.items() if v["desc"] == w["desc"]][0],
+        "tables": len(w["cards"]), "rows_per_rank": int(sum(w["cards"])), "dim": w["dim"],
+        "bitwidth": w["bitwidth"], "ranges": "adaptive greedy" if w["adaptive"] else "naive min/max",
+        "lookups": w["lookups"], "lookups_per_step_per_rank": int(w["n_per_table"] * len(w["cards"])),
         "lookup_dtype": "per table: u8 (<=256 rows), u16 (<=65536), i32 (above)",
         "scope": "interval (consecutive increments)",
-        "row_map": "Zipf rank -> row through a seeded permutation per table",
-        "l2": "flushed between timed steps (256 MB write; L2 126 MB); inputs 2.16 GB tables "
-              "+ a 61 MB packed lookup stream per step and rank",
+        "row_map": "Zipf rank -> row through a seeded permutation per table"
+                   if w["lookups"] == "zipf" else "uniform row ids",
+        "l2": "flushed between timed steps (256 MB write; L2 126 MB); tables and the packed "
+              "lookup stream are both larger than L2",
     }
 
 
@@ -131,8 +165,10 @@ class ClockSampler:
 # synthetic workload
 # --------------------------------------------------------------------------------
 
-def zipf_lookups_torch(rows, n, gen, device):
+def lookups_torch(kind, rows, n, gen, device):
     import torch
+    if kind == "uniform":
+        return torch.randint(0, rows, (n,), generator=gen, device=device, dtype=torch.int32)
     w = torch.arange(1, rows + 1, dtype=torch.float64, device=device).pow_(-ZIPF_S)
     cdf = torch.cumsum(w, 0)
     cdf /= cdf[-1].clone()
@@ -142,7 +178,9 @@ def zipf_lookups_torch(rows, n, gen, device):
     return perm[ranks].to(torch.int32)
 
 
-def zipf_lookups_numpy(rows, n, rng):
+def lookups_numpy(kind, rows, n, rng):
+    if kind == "uniform":
+        return rng.integers(0, rows, n).astype(np.int32)
     w = np.arange(1, rows + 1, dtype=np.float64) ** -ZIPF_S
     cdf = np.cumsum(w)
     cdf /= cdf[-1]
@@ -164,8 +202,9 @@ class CpuPath:
     releases the GIL); rows of a section run on OpenMP threads.
     """
 
-    def __init__(self, tables, lookups, cards, threads):
+    def __init__(self, tables, lookups, cards, threads, bitwidth=8, adaptive=None):
         from oracle import oracle as O
+        self.bitwidth, self.adaptive = bitwidth, adaptive
         self.O = O
         self.tables, self.lookups, self.cards = tables, lookups, cards
         self.threads = threads
@@ -174,9 +213,15 @@ class CpuPath:
         from concurrent.futures import ThreadPoolExecutor
         self.pool = ThreadPoolExecutor(max_workers=threads)
 
-    def step(self, tables_subset=None):
+    def step(self, tables_subset=None, max_build_rows=None):
+        """One interval: returns (dirty rows, payload bytes built, seconds).
+
+        With max_build_rows the sections are built for an evenly strided
+        sample of the dirty rows and the build time is scaled to all of them
+        (rows are independent in the reference codec, quant.py:14-15)."""
         O = self.O
         ts = range(len(self.cards)) if tables_subset is None else tables_subset
+        t0 = time.perf_counter()
 
         def track(t):
             O.mark(self.bits[t], self.cards[t], self.lookups[t])
@@ -185,20 +230,55 @@ class CpuPath:
             self.bits[t][:] = 0
             return ids
 
-        ids = list(self.pool.map(track, ts))
+        ids_all = list(self.pool.map(track, ts))
+        t1 = time.perf_counter()
+        rows = sum(i.size for i in ids_all)
+        scale = 1.0
+        ids = ids_all
+        if max_build_rows and rows > max_build_rows:
+            stride = int(np.ceil(rows / max_build_rows))
+            ids = [i[::stride] for i in ids_all]
+            scale = rows / max(1, sum(i.size for i in ids))
         big = [k for k, t in enumerate(ts) if ids[k].size > 65536]
         small = [k for k, t in enumerate(ts) if ids[k].size <= 65536]
 
         def build(k, nthreads):
             t = list(ts)[k]
-            return O.build_section(t, self.tables[t], ids[k], bitwidth=BITWIDTH, adaptive=None,
+            return O.build_section(t, self.tables[t], ids[k], bitwidth=self.bitwidth,
+                                   adaptive=self.adaptive,
                                    nthreads=nthreads)
 
         outs = list(self.pool.map(lambda k: build(k, 1), small))
         for k in big:
             outs.append(build(k, self.threads))
-        rows = sum(i.size for i in ids)
-        return rows, sum(len(o[0]) for o in outs)
+        t2 = time.perf_counter()
+        return rows, sum(len(o[0]) for o in outs), (t1 - t0) + (t2 - t1) * scale
+
+
+def cpu_measure(w, tables, lookups, budget_s=20.0, steps=None):
+    """The reference CPU path (oracle port) on all host threads: GB/s of
+    checkpointed rows over whole intervals (C2) or, for the large workloads,
+    intervals whose section build is sampled to ~budget_s."""
+    threads = os.cpu_count() or 1
+    acfg = {2: (25, 0.5), 3: (25, 0.2), 4: (45, 0.2)}.get(w["bitwidth"]) if w["adaptive"] else None
+    cp = CpuPath(tables, lookups, w["cards"], threads, w["bitwidth"], acfg)
+    big = sum(w["cards"]) > 50_000_000 or w["adaptive"]
+    cap = (200_000 if w["adaptive"] else 2_000_000) if big else None
+    cp.step(max_build_rows=cap)  # warm-up (page-in, OpenMP pool)
+    rows_c, secs, reps = 0, 0.0, 0
+    t0 = time.perf_counter()
+    while (steps is None and (reps == 0 or (reps < 3 and time.perf_counter() - t0 < budget_s))) \
+            or (steps is not None and reps < steps):
+        r, _, dt = cp.step(max_build_rows=cap)
+        rows_c += r
+        secs += dt
+        reps += 1
+    sample = (f"{reps} full interval(s): mark {int(sum(len(l) for l in lookups))} lookups, "
+              f"capture, {'adaptive' if w['adaptive'] else 'naive'} {w['bitwidth']}-bit sections of "
+              + ("every dirty row" if cap is None else f"a strided sample of {cap} dirty rows "
+                 "(build time scaled to all dirty rows)"))
+    return {"value": rows_c * w["dim"] * 4 / secs / 1e9, "unit": "GB/s", "cores": threads,
+            "kind": "port", "sample": sample, "seconds": secs, "steps": reps}
 
 
 def pack_lookups_device(lookups, cards, dev):
@@ -222,30 +302,20 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cards = CRITEO_KAGGLE[:args.tables]
+    w = workload_of(args)
+    cards = w["cards"]
     rng = np.random.default_rng(args.seed)
-    tables = [(rng.random((r, DIM), dtype=np.float32) * 2 - 1) for r in cards]
-    n_look = BATCHES * BATCH
-    lookups = [zipf_lookups_numpy(r, n_look, rng) for r in cards]
-    threads = os.cpu_count() or 1
-    cpu = CpuPath(tables, lookups, cards, threads)
-    for _ in range(max(1, args.warmup)):
-        cpu.step()
-    t0 = time.perf_counter()
-    rows_total = 0
-    for _ in range(args.steps):
-        rows, _ = cpu.step()
-        rows_total += rows
-    dt = time.perf_counter() - t0
-    value = rows_total * DIM * 4 / dt / 1e9
+    tables = [(rng.random((r, w["dim"]), dtype=np.float32) * 2 - 1) for r in cards]
+    lookups = [lookups_numpy(w["lookups"], r, w["n_per_table"], rng) for r in cards]
+    cpu = cpu_measure(w, tables, lookups, steps=max(1, args.steps))
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": workload_desc(cards, n_look),
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": "full C2 interval per step (all 26 tables, 26.6M lookups)"},
+        "n_gpus": args.gpus, "steps": cpu["steps"], "warmup": 1,
+        "ms_per_step": cpu["seconds"] / cpu["steps"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+        "config": workload_desc(w),
+        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -271,19 +341,24 @@ def run_ours(args):
         dslib.check(dslib.lib().ds_set_l2_fetch_granularity(args.l2_fetch), "l2 fetch")
     l2_fetch = int(dslib.lib().ds_get_l2_fetch_granularity())
 
-    cards = CRITEO_KAGGLE[:args.tables]
-    n_look = BATCHES * BATCH
+    w = workload_of(args)
+    cards, DIM = w["cards"], w["dim"]
+    n_look = w["n_per_table"]
     gen = torch.Generator(device=dev)
     gen.manual_seed(args.seed * 7919 + rank)
     tables = []
     for t, r in enumerate(cards):
         v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
         tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
-    lookups = [zipf_lookups_torch(r, n_look, gen, dev) for r in cards]
+    lookups = [lookups_torch(w["lookups"], r, n_look, gen, dev) for r in cards]
     # the interval's lookup stream, each table at its narrowest id width
     # (u8 <= 256 rows, u16 <= 65536, i32 above): ds_mark_packed's input
     stream = pack_lookups_device(lookups, cards, dev)
-    ck = ShardedCheckpointer(tables, BITWIDTH, rank=rank, world_size=world, device=dev)
+    # ranges: the reference's default for the bitwidth (engine.py:112-115),
+    # or naive min/max when the workload says so
+    overrides = None if w["adaptive"] else {w["bitwidth"]: None}
+    ck = ShardedCheckpointer(tables, w["bitwidth"], adaptive_overrides=overrides, rank=rank,
+                             world_size=world, device=dev)
     torch.cuda.synchronize()
 
     def barrier():
@@ -364,10 +439,10 @@ def run_ours(args):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(dom)
-    # (d=16, 8-bit: pick_cfg -> G=1 lane per row, C=4 x float4, naive mode 1)
-    roofline = {"bound": "hbm", "kernel": {"mark": "ds::mark_tma_kernel<int>",
-                                           "write": "ds::writer_warp_kernel<1,4,4,1,false>"}[dom],
+        traffic = json.load(open(tpath)).get(args.workload, {}).get(dom)
+    wk = ("ds::writer_kernel (adaptive greedy, compute-bound)" if w["adaptive"]
+          else "ds::writer_warp_kernel (naive ranges)")
+    roofline = {"bound": "hbm", "kernel": {"mark": "ds::mark_tma_kernel", "write": wk}[dom],
                 "measured_over": {"mark": "the mark phase (one mark_tma launch per step)",
                                   "write": "the write phase (one writer launch per step)"}[dom],
                 "traffic_source": "profiles/traffic.json: dram read+write bytes per launch, "
@@ -412,27 +487,16 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         host_tables = [t.values.cpu().numpy() for t in tables]
         host_look = [lk.cpu().numpy() for lk in lookups]
-        threads = os.cpu_count() or 1
-        cp = CpuPath(host_tables, host_look, cards, threads)
-        cp.step()
-        t0 = time.perf_counter()
-        rows_c, reps = 0, 0
-        while reps < 3 and (reps == 0 or time.perf_counter() - t0 < 20):
-            r, _ = cp.step()
-            rows_c += r
-            reps += 1
-        dt = time.perf_counter() - t0
-        cpu = {"value": rows_c * row_bytes / dt / 1e9, "unit": "GB/s", "cores": threads,
-               "kind": "port",
-               "sample": f"{reps} full C2 interval(s): mark 26.6M lookups, capture, "
-                         "8-bit sections of every dirty row"}
+        del lookups
+        c = cpu_measure(w, host_tables, host_look)
+        cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": elapsed / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-            "config": dict(workload_desc(cards, n_look), dirty_rows_per_step=dirty_all,
+            "config": dict(workload_desc(w), dirty_rows_per_step=dirty_all,
                            parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch),
             "rows_per_s": dirty_all * K / elapsed,
             "roofline": roofline, "phases": phases,

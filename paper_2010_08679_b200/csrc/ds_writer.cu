@@ -6,10 +6,37 @@
 
 namespace ds {
 
-// warp-tiles of the MODE 0/1 writer for `rows` records of dim `dim`
+// MODE 0/1 writer tiles: 32 records, fewer for huge records (keeping at
+// least ns-1 chunks of 32/G rows per tile); then fewer warps per CTA
+struct WarpPlan {
+    int tr, threads;
+    size_t smem;
+};
+static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c) {
+    const int rpc = 32 / c.G;
+    const int ns = c.G == 1 ? 2 : 3;  // writer_stages<G>()
+    auto warp_bytes = [&](int trr) {
+        return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) + (size_t)ns * align16(rpc * d * 4);
+    };
+    WarpPlan p;
+    p.tr = 32;
+    while (warp_bytes(p.tr) * (WT / 32) > 200 * 1024 && p.tr / 2 >= rpc * (ns - 1) && p.tr > 1) p.tr /= 2;
+    p.threads = WT;
+    while (warp_bytes(p.tr) * (p.threads / 32) > 200 * 1024 && p.threads > 32) p.threads /= 2;
+    p.smem = warp_bytes(p.tr) * (p.threads / 32) + 16;  // + alignment slack
+    return p;
+}
+
+// tiles of the MODE 0/1 writer for `rows` records of dim `dim` (any record
+// layout of that dim: sized with the largest, fp32 + aux + row ids)
 static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
-    const int rpw = 32 / pick_cfg((int)dim, dim % 4 == 0).G;
-    return rows / rpw + ntables + 1;
+    int tr = 32;
+    for (int v = 0; v < 2; v++) {  // float4 or scalar layout, whichever the call picks
+        if (v == 1 && dim % 4) continue;
+        const WarpPlan p = warp_plan((int)dim, 8 + 8 * dim, pick_cfg((int)dim, v == 1));
+        tr = p.tr < tr ? p.tr : tr;
+    }
+    return rows / tr + ntables + 1;
 }
 
 }  // namespace ds
@@ -105,15 +132,16 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     if (!fn) return host::fail(DS_ERR_CONFIG, "ds_write_payload: no kernel for this dim");
 
     int tr;
+    int threads = WT;
     size_t smem;
     if (mode != 2) {
-        // warp pipeline: tiles of 32/G records, per-warp stage + codes + 2 row
-        // buffers + 3 id buffers (writer_warp_kernel computes the same layout)
-        const int rpw = 32 / c.G;
-        tr = rpw;
-        const size_t warp_b = (size_t)align16(rpw * a.rec) + 16 + align16(rpw * d) +
-                              2 * (size_t)align16(rpw * d * 4) + 3 * (size_t)rpw * 8;
-        smem = warp_b * (WT / 32) + 16;  // + alignment slack
+        // warp pipeline: tiles of 32 records, per-warp record stage + codes
+        // scratch + a ring of NS row chunks of 32/G rows (writer_warp_kernel
+        // computes the same layout)
+        const WarpPlan wp = warp_plan(d, a.rec, c);
+        tr = wp.tr;
+        threads = wp.threads;
+        smem = wp.smem;
     } else {
         const int rpp = WT / c.G;  // one pass of rows per tile (compute-bound)
         tr = rpp;
@@ -129,10 +157,11 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         // incremental counts live on the device; bound by table rows
         max_tiles += (tables_host[t].rows + tr - 1) / tr;
     }
+    if (mode != 2) max_tiles = (max_tiles + threads / 32 - 1) / (threads / 32);  // warps -> CTAs
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
     if (per_sm < 1) per_sm = 1;
     int64_t grid = max_tiles < (int64_t)host::sm_count() * per_sm ? max_tiles
                                                                  : (int64_t)host::sm_count() * per_sm;
@@ -140,6 +169,6 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     if (grid > 4096) grid = 4096;
 
     // one launch: layout, records, exact fixups and the error sum
-    fn<<<(unsigned)grid, WT, smem, (cudaStream_t)stream>>>(a);
+    fn<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(a);
     return host::check_launch("ds_write_payload");
 }

@@ -62,6 +62,12 @@ struct WriterArgs {
 __device__ __forceinline__ void st_bytes(uint8_t *p, uint64_t v, int n) {
     for (int i = 0; i < n; i++) p[i] = (uint8_t)(v >> (8 * i));
 }
+// misaligned record layouts only (odd record sizes): out of line, so the
+// aligned stores of the common layouts stay real branches, not predicated
+// byte-store sequences
+static __device__ __noinline__ void st_bytes_slow(uint8_t *p, uint64_t v, int n) {
+    for (int i = 0; i < n; i++) p[i] = (uint8_t)(v >> (8 * i));
+}
 __device__ __forceinline__ void st_u32(uint8_t *p, uint32_t v) {
     if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) *reinterpret_cast<uint32_t *>(p) = v;
     else st_bytes(p, v, 4);
@@ -159,11 +165,12 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
     const int L = a.L;
     const int64_t gid = td.row_base + local;
     bool fix = false;  // MODE 1: row left to the exact fixup pass (fix_tile)
+    // record fields 8-byte aligned (stages are 16-byte aligned, so every
+    // record of a stage then is): warp-uniform
+    const bool al8 = (((unsigned)a.rec | (unsigned)a.par_off | (unsigned)a.code_off) & 7u) == 0u;
     if (valid && a.incremental && lig == 0) {
-        if ((reinterpret_cast<uintptr_t>(rec) & 7) == 0)
-            *reinterpret_cast<uint64_t *>(rec) = (uint64_t)gid;
-        else
-            st_bytes(rec, (uint64_t)gid, 8);
+        if (al8) *reinterpret_cast<uint64_t *>(rec) = (uint64_t)gid;
+        else st_bytes_slow(rec, (uint64_t)gid, 8);
     }
     if (MODE == 0) {
         if (valid) {
@@ -245,8 +252,11 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
             // diagnostic sum whose low bits depend on summation order anyway)
             acc.err += sse > 0.0 ? sse * rsqrt(sse) : 0.0;
             acc.n_rows++;
-            st_u32(rec + a.par_off, __float_as_uint(lo));
-            st_u32(rec + a.par_off + 4, __float_as_uint(hi));
+            if (al8)
+                *reinterpret_cast<uint2 *>(rec + a.par_off) = make_uint2(__float_as_uint(lo), __float_as_uint(hi));
+            else
+                st_bytes_slow(rec + a.par_off,
+                              ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo), 8);
         }
         // ---- pack (quant.py:376-382): LSB-first bitstream ----
         uint8_t *pk = rec + a.code_off;
@@ -260,11 +270,13 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
                         if (a.bitwidth == 8) {
                             v = q[4 * c] | (q[4 * c + 1] << 8) | (q[4 * c + 2] << 16) |
                                 ((uint32_t)q[4 * c + 3] << 24);
-                            st_u32(pk + 4 * m, v);
+                            if (al8) *reinterpret_cast<uint32_t *>(pk + 4 * m) = v;
+                            else st_bytes_slow(pk + 4 * m, v, 4);
                         } else if (a.bitwidth == 4) {
                             v = q[4 * c] | (q[4 * c + 1] << 4) | (q[4 * c + 2] << 8) |
                                 (q[4 * c + 3] << 12);
-                            st_bytes(pk + 2 * m, v, 2);
+                            if (al8) *reinterpret_cast<uint16_t *>(pk + 2 * m) = (uint16_t)v;
+                            else st_bytes_slow(pk + 2 * m, v, 2);
                         } else {
                             v = q[4 * c] | (q[4 * c + 1] << 2) | (q[4 * c + 2] << 4) |
                                 (q[4 * c + 3] << 6);
@@ -403,7 +415,7 @@ __device__ __forceinline__ void writer_epilogue(const WriterArgs &a, WAcc &acc, 
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int w = 0; w < WT / 32; w++) s += s_red[w];
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += s_red[w];
         a.partials[blockIdx.x] = s;
         __threadfence();
         s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
@@ -444,18 +456,16 @@ __device__ __forceinline__ int tile_table(const int64_t *s_sched, int nt, int64_
 // ---------------------------------------------------------------------------
 template <int G, int C, int VEC, bool PAD>
 __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_sched,
-                                         const int64_t *s_sec, int64_t tile,
+                                         const int64_t *s_sec, int t, int64_t i0,
                                          unsigned m, uint8_t *cs_warp, int d, WAcc &acc) {
+    // rows i0 + slot of table t whose bit slot is set in m
     using Lay = Layout<G, C, VEC>;
     constexpr int EPL = C * VEC;
-    constexpr int RPW = 32 / G;
     const int lane = threadIdx.x & 31;
     const int lig = lane & (G - 1), slot = lane / G;
     const int nt = a.ntables;
-    const int t = tile_table(s_sched, nt, tile, lane);
     const ds_table_desc &td = a.t[t];
-    const int64_t i0 = (tile - s_sched[t]) * RPW;
-    const bool mine = (m >> (slot * G)) & 1u;
+    const bool mine = (m >> slot) & 1u;
     uint8_t *cs = cs_warp + slot * d;
     int64_t local = 0;
     if (mine) {
@@ -540,160 +550,182 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
 }
 
 // ---------------------------------------------------------------------------
-// MODE 0/1: HBM-bound gather.  Every warp runs its own pipeline over
-// warp-tiles of 32/G consecutive records (no CTA barriers): the ids of tile
-// k+2 and the rows of tile k+1 are in flight (cp.async groups into the warp's
-// shared memory) while tile k is coded into the warp's record stage, which
-// then streams to HBM as one contiguous run.
+// MODE 0/1: HBM-bound gather.  Every warp runs its own pipeline (no CTA
+// barriers) over tiles of 32 records: one dirty-row id per lane, loaded two
+// tiles ahead into registers; the tile's rows move in G chunks of 32/G rows
+// (a chunk = one row per group of G lanes) through a ring of NS cp.async
+// stages in the warp's shared memory, NS-1 chunks ahead of the chunk being
+// coded into the tile's record stage; the 32 records then stream to HBM as
+// one contiguous run.  Per-tile bookkeeping is amortised over 32 rows at
+// every dim.
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int align16(int v) { return (v + 15) & ~15; }
 
+#ifndef DS_WRITER_MINB
+#define DS_WRITER_MINB 3
+#endif
+template <int G>
+__host__ __device__ constexpr int writer_stages() { return G == 1 ? 2 : 3; }
+
 template <int G, int C, int VEC, int MODE, bool PAD>
-__global__ void __launch_bounds__(WT, 3) writer_warp_kernel(const WriterArgs a) {
+__global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const WriterArgs a) {
     constexpr int EPL = C * VEC;
-    constexpr int RPW = 32 / G;  // records per warp-tile
+    constexpr int RPC = 32 / G;  // rows per chunk
+    constexpr int NS = writer_stages<G>();
+    const int TR = a.tile_rows;  // records per tile: 32, fewer for huge records (host)
+    const int NCH = TR / RPC;    // chunks per tile (the host keeps NCH >= NS - 1)
     extern __shared__ __align__(16) uint8_t smem[];
     const int d = PAD ? a.dim : (VEC == 4 ? 4 * G * C : G * C);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int lig = lane & (G - 1);
-    const int slot = lane / G;  // record of the warp-tile this group codes
-    // per-warp shared memory (host computes the same sizes)
-    const int stage_b = align16(RPW * a.rec) + 16;
-    const int codes_b = align16(RPW * d);
-    const int rows_b = align16(RPW * d * 4);
-    const int warp_b = stage_b + codes_b + 2 * rows_b + 3 * RPW * 8;
-    // 16-byte aligned carve-up whatever the static shared memory in front
+    const int slot = lane / G;  // row of the chunk this group codes
+    // per-warp shared memory (the host computes the same sizes)
+    const int stage_b = align16(TR * a.rec) + 16;
+    const int codes_b = align16(RPC * d);
+    const int chunk_b = align16(RPC * d * 4);
+    const int warp_b = stage_b + codes_b + NS * chunk_b;
     uint8_t *smem_al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 15) & ~(uintptr_t)15);
     uint8_t *wbase = smem_al + (size_t)wid * warp_b;
     uint8_t *stage = wbase;
     uint8_t *codes = wbase + stage_b;
-    float *rows_sh = reinterpret_cast<float *>(codes + codes_b);
-    int64_t *ids_sh = reinterpret_cast<int64_t *>(codes + codes_b + 2 * rows_b);
+    float *ring = reinterpret_cast<float *>(codes + codes_b);
 
     __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
     __shared__ double s_red[WT / 32];
-    const int nt = a.ntables;
     __shared__ int64_t s_sec[DS_MAX_TABLES + 1];
     writer_layout(a, s_sched, s_sec);
+    const int nt = a.ntables;
     WAcc acc;
     if (s_sec[nt] <= a.capacity) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
         const int64_t total_tiles = s_sched[nt];
-        const int64_t gw = (int64_t)blockIdx.x * (WT / 32) + wid;
-        const int64_t nwarps = (int64_t)gridDim.x * (WT / 32);
-        // tile k of this warp -> (table, first record, records); each tile is
-        // looked up once and carried through a 3-deep ring (ids k+2, rows k+1,
-        // coding k)
+        const int nwc = blockDim.x >> 5;  // warps per CTA (fewer for huge records)
+        const int64_t gw = (int64_t)blockIdx.x * nwc + wid;
+        const int64_t nwarps = (int64_t)gridDim.x * nwc;
+        // tile j of this warp: table, first record, records, and lane's row id
         struct TI {
             int t, nrow;
-            int64_t i0;
+            int64_t i0, loc;  // loc: table-local row of record `lane` (-1: none / invalid)
             bool ok;
         };
-        auto info = [&](int k) -> TI {
+        auto tinfo = [&](int j) -> TI {
             TI r;
-            const int64_t tile = gw + (int64_t)k * nwarps;
+            const int64_t tile = gw + (int64_t)j * nwarps;
             r.ok = tile < total_tiles;
             r.t = r.ok ? tile_table(s_sched, nt, tile, lane) : 0;
-            r.i0 = r.ok ? (tile - s_sched[r.t]) * RPW : 0;
-            r.nrow = r.ok ? (int)min((int64_t)RPW, s_sched[nt + 1 + r.t] - r.i0) : 0;
+            r.i0 = r.ok ? (tile - s_sched[r.t]) * TR : 0;
+            r.nrow = r.ok ? (int)min((int64_t)TR, s_sched[nt + 1 + r.t] - r.i0) : 0;
+            r.loc = -1;
+            if (lane < r.nrow) {
+                const ds_table_desc &td = a.t[r.t];
+                int64_t loc = r.i0 + lane;
+                if (a.incremental) {  // ids from capture are table-local; plan ids are global
+                    const int64_t raw = a.ids[s_sched[2 * nt + 1 + r.t] + r.i0 + lane];
+                    loc = a.ids_local ? raw : raw - td.row_base;
+                }
+                r.loc = (loc < 0 || loc >= td.rows) ? -2 : loc;  // -2: out of range
+            }
             return r;
         };
-        auto local_of = [&](const ds_table_desc &td, int64_t raw) -> int64_t {
-            // ids from capture are table-local; plan ids are global
-            int64_t local = a.ids_local ? raw : raw - td.row_base;
-            return (local < 0 || local >= td.rows) ? -1 : local;
-        };
-        auto issue_ids = [&](const TI &ti, int k) {
-            if (a.incremental && ti.ok && lane < ti.nrow)
-                cp_async8(ids_sh + (k % 3) * RPW + lane,
-                          a.ids + s_sched[2 * nt + 1 + ti.t] + ti.i0 + lane);
-            cp_async_commit();
-        };
-        auto issue_rows = [&](const TI &ti, int k) {
-            if (ti.ok && slot < ti.nrow) {
-                const ds_table_desc &td = a.t[ti.t];
-                const int64_t local = a.incremental ? local_of(td, ids_sh[(k % 3) * RPW + slot])
-                                                    : ti.i0 + slot;
-                if (local >= 0) {
-                    const float *src = td.values + local * td.ld;
-                    float *dst = rows_sh + (k & 1) * (rows_b / 4) + slot * d;
+        // chunk `sub` of tile T into ring stage st (one row per lane group)
+        auto issue = [&](const TI &T, int sub, int st) {
+            const int r = sub * RPC + slot;
+            const int64_t loc = __shfl_sync(DS_FULL_MASK, T.loc, r);
+            if (T.ok && r < T.nrow && loc >= 0) {
+                const ds_table_desc &td = a.t[T.t];
+                const float *src = td.values + loc * td.ld;
+                float *dst = ring + st * (chunk_b / 4) + slot * d;
 #pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        if (VEC == 4) {
-                            int e = 4 * (lig + c * G);
-                            if (e < d) cp_async16(dst + e, src + e);
-                        } else {
-                            int e = lig + c * G;
-                            if (e < d) cp_async4(dst + e, src + e);
-                        }
+                for (int c = 0; c < C; c++) {
+                    if (VEC == 4) {
+                        const int e = 4 * (lig + c * G);
+                        if (e < d) cp_async16(dst + e, src + e);
+                    } else {
+                        const int e = lig + c * G;
+                        if (e < d) cp_async4(dst + e, src + e);
                     }
                 }
             }
             cp_async_commit();
         };
-        // prologue: ids(0) landed; ids(1) and rows(0) in flight
-        TI cur = info(0), nxt = info(1);
-        issue_ids(cur, 0);
-        cp_async_wait<0>();
-        __syncwarp();
-        issue_ids(nxt, 1);
-        issue_rows(cur, 0);
-        for (int k = 0; cur.ok; k++) {
-            const TI far = info(k + 2);
+        TI cur = tinfo(0), nxt = tinfo(1);
+        // prologue: the first NS-1 chunks of the warp's chunk stream
+        int isub = 0, irel = 0, ist = 0;  // next chunk to issue: sub-chunk, tile (0 cur, 1 nxt), stage
+#pragma unroll
+        for (int cc = 0; cc < NS - 1; cc++) {
+            issue(irel == 0 ? cur : nxt, isub, ist);
+            ist++;
+            if (++isub == NCH) { isub = 0; irel++; }
+        }
+        int cst = 0;  // ring stage of the chunk being coded
+        for (int j = 0; cur.ok; j++) {
+            const TI far = tinfo(j + 2);  // ids two tiles ahead (plain loads, consumed a tile later)
             const ds_table_desc &td = a.t[cur.t];
-            cp_async_wait<1>();  // ids(k+1) landed (rows(k) may still be in flight)
-            __syncwarp();
-            issue_ids(far, k + 2);
-            issue_rows(nxt, k + 1);
-            cp_async_wait<2>();  // rows(k) landed: each lane reads only its own copies
-            const int nrow = cur.nrow;
-            const int64_t i0 = cur.i0;
-            bool valid = slot < nrow;
-            int64_t local = 0;
-            if (valid) {
-                local = a.incremental ? local_of(td, ids_sh[(k % 3) * RPW + slot]) : i0 + slot;
-                if (local < 0) {
+            bool row_fix = false;  // lane r: record r of the tile goes to the fixup pass
+#pragma unroll 1
+            for (int sub = 0; sub < NCH; sub++) {
+                // keep NS-1 chunks in flight
+                issue(irel == 0 ? cur : nxt, isub, ist);
+                ist = ist + 1 == NS ? 0 : ist + 1;
+                if (++isub == NCH) { isub = 0; irel++; }
+                cp_async_wait<NS - 1>();  // this chunk landed (each lane reads only its own copies)
+                const int r = sub * RPC + slot;
+                const int64_t loc = __shfl_sync(DS_FULL_MASK, cur.loc, r);
+                bool valid = r < cur.nrow;
+                if (valid && loc < 0) {
                     acc.bad_ids = true;
                     valid = false;
-                    local = 0;
                 }
-            }
-            float x[EPL];
-            const float *row = rows_sh + (k & 1) * (rows_b / 4) + slot * d;
-            if (VEC == 4) {
+                float x[EPL];
+                const float *row = ring + cst * (chunk_b / 4) + slot * d;
+                if (VEC == 4) {
 #pragma unroll
-                for (int c = 0; c < C; c++) {
-                    int e = 4 * (lig + c * G);
-                    float4 v = (valid && e < d) ? *reinterpret_cast<const float4 *>(row + e)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
-                    x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-                }
-            } else {
+                    for (int cv = 0; cv < C; cv++) {
+                        const int e = 4 * (lig + cv * G);
+                        const float4 v = (valid && e < d) ? *reinterpret_cast<const float4 *>(row + e)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                        x[4 * cv] = v.x; x[4 * cv + 1] = v.y; x[4 * cv + 2] = v.z; x[4 * cv + 3] = v.w;
+                    }
+                } else {
 #pragma unroll
-                for (int kk = 0; kk < C; kk++) {
-                    int e = lig + kk * G;
-                    x[kk] = (valid && e < d) ? row[e] : 0.f;
+                    for (int kk = 0; kk < C; kk++) {
+                        const int e = lig + kk * G;
+                        x[kk] = (valid && e < d) ? row[e] : 0.f;
+                    }
                 }
+                const bool fix = code_row<G, C, VEC, MODE, PAD>(a, td, x, row, valid, valid ? loc : 0,
+                                                                stage + r * a.rec, codes + slot * d,
+                                                                nullptr, lig, d, acc);
+                if (MODE == 1) {  // record r's flag to lane r
+                    const bool f = __shfl_sync(DS_FULL_MASK, fix, ((lane - sub * RPC) & (RPC - 1)) * G);
+                    if (lane >= sub * RPC && lane < (sub + 1) * RPC) row_fix |= f;
+                }
+                __syncwarp();  // every lane is done with ring stage cst before it is refilled
+                cst = cst + 1 == NS ? 0 : cst + 1;
             }
-            const bool fix = code_row<G, C, VEC, MODE, PAD>(a, td, x, row, valid, local,
-                                                            stage + slot * a.rec, codes + slot * d,
-                                                            nullptr, lig, d, acc);
-            // rows for the fixup pass below: one bit per group leader lane
-            const unsigned fixm = __ballot_sync(DS_FULL_MASK, fix && lig == 0);
-            if (MODE == 1 && lane == 0) a.fix_mask[gw + (int64_t)k * nwarps] = fixm;
-            __syncwarp();
-            const int64_t dst = s_sec[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + i0 * a.rec;
-            copy_out(a.payload + dst, stage, (int64_t)nrow * a.rec, lane, 32);
+            irel--;  // the next tile becomes the current one
+            if (MODE == 1) {
+                const unsigned fm = __ballot_sync(DS_FULL_MASK, row_fix);
+                if (lane == 0) a.fix_mask[gw + (int64_t)j * nwarps] = fm;
+            }
+            const int64_t dst = s_sec[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + cur.i0 * a.rec;
+            copy_out(a.payload + dst, stage, (int64_t)cur.nrow * a.rec, lane, 32);
             __syncwarp();  // the stage is rewritten by the next tile
             cur = nxt;
             nxt = far;
         }
         cp_async_wait<0>();  // nothing may land after the warp exits
         if (MODE == 1) {
-            // exact re-coding of this warp's flagged rows (its tiles, in order)
+            // exact re-coding of this warp's flagged records (its tiles, in order)
             __syncwarp();
             for (int64_t tile = gw; tile < total_tiles; tile += nwarps) {
                 const unsigned m = a.fix_mask[tile];
-                if (m) fix_tile<G, C, VEC, PAD>(a, s_sched, s_sec, tile, m, codes, d, acc);
+                if (!m) continue;
+                const int t = tile_table(s_sched, nt, tile, lane);
+                const int64_t i0 = (tile - s_sched[t]) * TR;
+                for (int sub = 0; sub < NCH; sub++) {
+                    const unsigned ms = (m >> (sub * RPC)) & (RPC == 32 ? 0xffffffffu : ((1u << RPC) - 1u));
+                    if (ms) fix_tile<G, C, VEC, PAD>(a, s_sched, s_sec, t, i0 + sub * RPC, ms, codes, d, acc);
+                }
             }
         }
     }

@@ -9,6 +9,7 @@ sys.path.insert(0, os.path.dirname(__file__))
 import ncu_lines  # noqa: E402
 
 tag = sys.argv[1]
+workload = sys.argv[2] if len(sys.argv) > 2 else "C2"
 G = "gpurun_out"
 out = []
 b = json.load(open(f"{G}/bench.json"))
@@ -78,5 +79,9 @@ for r in R[2:]:
         out.append(f"(line attribution failed: {e})\n")
 os.makedirs("profiles", exist_ok=True)
 open(f"profiles/{tag}_summary.md", "w").write("\n".join(out) + "\n")
-json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
+tp = "profiles/traffic.json"
+allt = json.load(open(tp)) if os.path.exists(tp) else {}
+allt = {k: v for k, v in allt.items() if isinstance(v, dict)}  # per-workload entries
+allt[workload] = traffic
+json.dump(allt, open(tp, "w"), indent=1)
 print(f"wrote profiles/{tag}_summary.md", traffic)
