@@ -14,7 +14,7 @@ struct WarpPlan {
 };
 static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c) {
     const int rpc = 32 / c.G;
-    const int ns = c.G == 1 ? 2 : 3;  // writer_stages<G>()
+    const int ns = c.G == 1 ? 2 : DS_WRITER_NS;  // writer_stages<G>()
     auto warp_bytes = [&](int trr) {
         return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) + (size_t)ns * align16(rpc * d * 4);
     };
@@ -33,7 +33,7 @@ static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
     int tr = 32;
     for (int v = 0; v < 2; v++) {  // float4 or scalar layout, whichever the call picks
         if (v == 1 && dim % 4) continue;
-        const WarpPlan p = warp_plan((int)dim, 8 + 8 * dim, pick_cfg((int)dim, v == 1));
+        const WarpPlan p = warp_plan((int)dim, 8 + 8 * dim, pick_cfg((int)dim, v == 1, 1));
         tr = p.tr < tr ? p.tr : tr;
     }
     return rows / tr + ntables + 1;
@@ -122,8 +122,8 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     a.flags = flags;
     a.stats = p->stats;
 
-    Cfg c = pick_cfg(d, vec4);
     const int mode = bw == 0 ? 0 : (p->adaptive_bins > 0 ? 2 : 1);
+    Cfg c = pick_cfg(d, vec4, mode);
     const bool pad = (c.VEC == 4 ? 4 * c.G * c.C : c.G * c.C) != d;
     writer_fn fn = nullptr;
     if (mode == 0) fn = select_writer_mode0(c, pad);

@@ -562,10 +562,13 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
 __host__ __device__ constexpr int align16(int v) { return (v + 15) & ~15; }
 
 #ifndef DS_WRITER_MINB
-#define DS_WRITER_MINB 3
+#define DS_WRITER_MINB 2
+#endif
+#ifndef DS_WRITER_NS
+#define DS_WRITER_NS 3
 #endif
 template <int G>
-__host__ __device__ constexpr int writer_stages() { return G == 1 ? 2 : 3; }
+__host__ __device__ constexpr int writer_stages() { return G == 1 ? 2 : DS_WRITER_NS; }
 
 template <int G, int C, int VEC, int MODE, bool PAD>
 __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const WriterArgs a) {
@@ -818,12 +821,18 @@ static int next_pow2(int v) {
     return p;
 }
 
-static Cfg pick_cfg(int d, bool vec4) {
+#ifndef DS_EPL_NAIVE
+#define DS_EPL_NAIVE 16
+#endif
+// mode 2 (greedy search) keeps ~16 elements per lane (register-bound); the
+// HBM-bound naive/fp32 writer amortises per-row work over DS_EPL_NAIVE
+static Cfg pick_cfg(int d, bool vec4, int mode = 2) {
     Cfg c;
+    const int epl = mode == 2 ? 16 : DS_EPL_NAIVE;
     if (vec4) {
         int chunks = d / 4;
         c.VEC = 4;
-        c.G = next_pow2((chunks + 3) / 4);
+        c.G = next_pow2((chunks + epl / 4 - 1) / (epl / 4));
         if (c.G > 32) c.G = 32;
         c.C = next_pow2((chunks + c.G - 1) / c.G);
     } else {
@@ -845,6 +854,9 @@ static writer_fn select_writer(const Cfg &c) {
     }
     DS_W(1, 1, 4) DS_W(1, 2, 4) DS_W(1, 4, 4) DS_W(2, 4, 4) DS_W(4, 4, 4) DS_W(8, 4, 4)
     DS_W(16, 4, 4) DS_W(32, 4, 4) DS_W(32, 8, 4)
+    if constexpr (MODE != 2) {
+        DS_W(1, 8, 4) DS_W(2, 8, 4) DS_W(4, 8, 4) DS_W(8, 8, 4) DS_W(16, 8, 4)
+    }
     DS_W(1, 1, 1) DS_W(1, 2, 1) DS_W(1, 4, 1) DS_W(1, 8, 1) DS_W(1, 16, 1) DS_W(2, 16, 1)
     DS_W(4, 16, 1) DS_W(8, 16, 1) DS_W(16, 16, 1) DS_W(32, 16, 1) DS_W(32, 32, 1)
 #undef DS_W
