@@ -16,7 +16,8 @@ static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c) {
     const int rpc = 32 / c.G;
     const int ns = c.G == 1 ? 2 : DS_WRITER_NS;  // writer_stages<G>()
     auto warp_bytes = [&](int trr) {
-        return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) + (size_t)ns * align16(rpc * d * 4);
+        return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) +
+               (size_t)ns * ((rpc * d * 4 + 63) & ~63);
     };
     WarpPlan p;
     p.tr = 32;

@@ -155,13 +155,16 @@ struct WAcc {
 // (wire layout of payload.py:84-104): [u64 row] [f32 lo, f32 hi, codes] |
 // [dim f32] [dim f32 aux].  `cs` is the group's dim-byte code scratch,
 // `buf` its exact-evaluation scratch (MODE 2).
-template <int G, int C, int VEC, int MODE, bool PAD>
+// CONTIG: lane lig holds elements [EPL*lig, EPL*lig + EPL) (the warp writer's
+// shared-memory row chunks); else the interleaved Layout<G, C, VEC> order.
+template <int G, int C, int VEC, int MODE, bool PAD, bool CONTIG = false>
 __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_desc &td,
                                          float (&x)[C * VEC], const float *xs, bool valid, int64_t local,
                                          uint8_t *rec, uint8_t *cs, double *buf, int lig, int d,
                                          WAcc &acc) {
     using Lay = Layout<G, C, VEC>;
     constexpr int EPL = C * VEC;
+    auto el = [&](int k) -> int { return CONTIG ? EPL * lig + k : Lay::elem(lig, k); };
     const int L = a.L;
     const int64_t gid = td.row_base + local;
     bool fix = false;  // MODE 1: row left to the exact fixup pass (fix_tile)
@@ -176,7 +179,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
         if (valid) {
 #pragma unroll
             for (int k = 0; k < EPL; k++) {
-                int e = Lay::elem(lig, k);
+                int e = el(k);
                 if (e < d) st_u32(rec + a.par_off + 4 * e, __float_as_uint(x[k]));
             }
         }
@@ -188,7 +191,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
         float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
         for (int k = 0; k < EPL; k++) {
-            if (!PAD || Lay::elem(lig, k) < d) {
+            if (!PAD || el(k) < d) {
                 mn = fmin_nan(mn, x[k]);
                 mx = fmax_nan(mx, x[k]);
             }
@@ -228,7 +231,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
                 // err_sum term (engine.py:171-173): exact dequantized value
                 const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf), (double)lo));
                 const double er = __dsub_rn((double)x[k], (double)dq);
-                if (!PAD || Lay::elem(lig, k) < d) sse = fma(er, er, sse);
+                if (!PAD || el(k) < d) sse = fma(er, er, sse);
             }
             dev = grp_max<G>(dev);  // every lane shuffles (no short-circuit)
             fix = row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps);
@@ -239,12 +242,12 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
                 q[k] = code_of(x[k], rq, acc.n_exact_codes);
                 const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)q[k]), (double)lo));
                 const double er = __dsub_rn((double)x[k], (double)dq);
-                if (!PAD || Lay::elem(lig, k) < d) sse = fma(er, er, sse);
+                if (!PAD || el(k) < d) sse = fma(er, er, sse);
             }
         }
 #pragma unroll
         for (int k = 0; k < EPL; k++)
-            if (!row_ok || (PAD && Lay::elem(lig, k) >= d)) q[k] = 0;  // padding codes are 0
+            if (!row_ok || (PAD && el(k) >= d)) q[k] = 0;  // padding codes are 0
         if (!row_ok) sse = 0.0;  // rejected rows add no error
         sse = grp_sumd<G>(sse);
         if (row_ok && lig == 0) {
@@ -260,11 +263,43 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
         }
         // ---- pack (quant.py:376-382): LSB-first bitstream ----
         uint8_t *pk = rec + a.code_off;
-        if (VEC == 4 && (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2)) {
+        if (CONTIG && VEC == 4 && !PAD && C == 4 && al8 &&
+            (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2)) {
+            // the lane's 16 contiguous codes -> one 16 / 8 / 4-byte store
+            if (valid) {
+                if (a.bitwidth == 8) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int c = 0; c < 4; c++)
+                        w[c] = q[4 * c] + (q[4 * c + 1] << 8) + (q[4 * c + 2] << 16) + ((uint32_t)q[4 * c + 3] << 24);
+                    if ((a.code_off & 15) == 0 && (a.rec & 15) == 0)
+                        *reinterpret_cast<uint4 *>(pk + 16 * lig) = make_uint4(w[0], w[1], w[2], w[3]);
+                    else {
+                        *reinterpret_cast<uint2 *>(pk + 16 * lig) = make_uint2(w[0], w[1]);
+                        *reinterpret_cast<uint2 *>(pk + 16 * lig + 8) = make_uint2(w[2], w[3]);
+                    }
+                } else if (a.bitwidth == 4) {
+                    uint32_t w[2];
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        uint32_t v = 0;
+#pragma unroll
+                        for (int j = 7; j >= 0; j--) v = (v << 4) + (uint32_t)q[8 * h + j];
+                        w[h] = v;
+                    }
+                    *reinterpret_cast<uint2 *>(pk + 8 * lig) = make_uint2(w[0], w[1]);
+                } else {
+                    uint32_t v = 0;
+#pragma unroll
+                    for (int j = 15; j >= 0; j--) v = (v << 2) + (uint32_t)q[j];
+                    *reinterpret_cast<uint32_t *>(pk + 4 * lig) = v;
+                }
+            }
+        } else if (VEC == 4 && (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2)) {
             if (valid) {
 #pragma unroll
                 for (int c = 0; c < C; c++) {
-                    int m = lig + c * G;  // chunk index: elements 4m..4m+3
+                    const int m = CONTIG ? C * lig + c : lig + c * G;  // chunk: elements 4m..4m+3
                     if (4 * m < d) {
                         uint32_t v;
                         if (a.bitwidth == 8) {
@@ -290,7 +325,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
             if (valid) {
 #pragma unroll
                 for (int k = 0; k < EPL; k++) {
-                    int e = Lay::elem(lig, k);
+                    int e = el(k);
                     if (e < d) cs[e] = (uint8_t)q[k];
                 }
             }
@@ -561,6 +596,12 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int align16(int v) { return (v + 15) & ~15; }
 
+// 16-byte chunk g of a row-chunk stage lives at slot g ^ ((g >> 3) & 3): the
+// 8 lanes of a quarter-warp then hit 8 distinct bank groups both when lane
+// lig reads chunks C*lig..C*lig+C-1 of its row and when consecutive lanes
+// write consecutive chunks (a permutation inside each aligned group of 4)
+__device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
+
 #ifndef DS_WRITER_MINB
 #define DS_WRITER_MINB 2
 #endif
@@ -585,13 +626,18 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
     // per-warp shared memory (the host computes the same sizes)
     const int stage_b = align16(TR * a.rec) + 16;
     const int codes_b = align16(RPC * d);
-    const int chunk_b = align16(RPC * d * 4);
+    const int chunk_b = (RPC * d * 4 + 63) & ~63;  // whole 4-chunk swizzle groups
     const int warp_b = stage_b + codes_b + NS * chunk_b;
     uint8_t *smem_al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 15) & ~(uintptr_t)15);
     uint8_t *wbase = smem_al + (size_t)wid * warp_b;
     uint8_t *stage = wbase;
     uint8_t *codes = wbase + stage_b;
     float *ring = reinterpret_cast<float *>(codes + codes_b);
+    // 16-byte chunk g of a stage: swizzled when each lane reads its own row
+    // (G == 1: rows 64 B apart would put 4 lanes on one bank group), natural
+    // otherwise (consecutive lanes already read consecutive chunks, and the
+    // cp.async writes stay contiguous)
+    auto slot_of = [](int g) -> int { return G == 1 ? chunk_swz(g) : g; };
 
     __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
     __shared__ double s_red[WT / 32];
@@ -637,11 +683,14 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
                 const ds_table_desc &td = a.t[T.t];
                 const float *src = td.values + loc * td.ld;
                 float *dst = ring + st * (chunk_b / 4) + slot * d;
+                float *sbase = ring + st * (chunk_b / 4);
 #pragma unroll
                 for (int c = 0; c < C; c++) {
                     if (VEC == 4) {
-                        const int e = 4 * (lig + c * G);
-                        if (e < d) cp_async16(dst + e, src + e);
+                        // global: consecutive lanes, consecutive 16 bytes; shared:
+                        // 16-byte chunk g of the stage at swizzled slot chunk_swz(g)
+                        const int q = lig + c * G;
+                        if (4 * q < d) cp_async16(sbase + 4 * slot_of(slot * (d >> 2) + q), src + 4 * q);
                     } else {
                         const int e = lig + c * G;
                         if (e < d) cp_async4(dst + e, src + e);
@@ -670,7 +719,7 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
                 issue(irel == 0 ? cur : nxt, isub, ist);
                 ist = ist + 1 == NS ? 0 : ist + 1;
                 if (++isub == NCH) { isub = 0; irel++; }
-                cp_async_wait<NS - 1>();  // this chunk landed (each lane reads only its own copies)
+                cp_async_wait<NS - 1>();  // this lane's copies of the chunk landed (it reads only those)
                 const int r = sub * RPC + slot;
                 const int64_t loc = __shfl_sync(DS_FULL_MASK, cur.loc, r);
                 bool valid = r < cur.nrow;
@@ -681,11 +730,15 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
                 float x[EPL];
                 const float *row = ring + cst * (chunk_b / 4) + slot * d;
                 if (VEC == 4) {
+                    // G == 1: the lane's own row, through the swizzle (conflict-free);
+                    // G > 1: chunk lig + cv*G (consecutive lanes, consecutive chunks)
+                    const float *sb = ring + cst * (chunk_b / 4);
 #pragma unroll
                     for (int cv = 0; cv < C; cv++) {
-                        const int e = 4 * (lig + cv * G);
-                        const float4 v = (valid && e < d) ? *reinterpret_cast<const float4 *>(row + e)
-                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const int q = G == 1 ? cv : lig + cv * G;
+                        const float4 v = (valid && 4 * q < d)
+                                             ? *reinterpret_cast<const float4 *>(sb + 4 * slot_of(slot * (d >> 2) + q))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
                         x[4 * cv] = v.x; x[4 * cv + 1] = v.y; x[4 * cv + 2] = v.z; x[4 * cv + 3] = v.w;
                     }
                 } else {
@@ -695,7 +748,7 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
                         x[kk] = (valid && e < d) ? row[e] : 0.f;
                     }
                 }
-                const bool fix = code_row<G, C, VEC, MODE, PAD>(a, td, x, row, valid, valid ? loc : 0,
+                const bool fix = code_row<G, C, VEC, MODE, PAD, VEC == 4 && G == 1>(a, td, x, row, valid, valid ? loc : 0,
                                                                 stage + r * a.rec, codes + slot * d,
                                                                 nullptr, lig, d, acc);
                 if (MODE == 1) {  // record r's flag to lane r
