@@ -364,6 +364,65 @@ __device__ __forceinline__ void eval_fast(const float (&x)[C * VEC], int d, int 
     B = 1.5f * b + 1e-37f;
 }
 
+// Both candidates of a greedy step in one pass over the row: two independent
+// accumulation chains per element (ILP), one loop over the registers.  Same
+// arithmetic and bounds as two eval_fast calls.
+template <int G, int C, int VEC, bool PAD>
+__device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int lig, float loA,
+                                           float hiA, float loB, float hiB, int L, float &SA,
+                                           float &BA, float &SB, float &BB) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    const float rngA = __fsub_rn(hiA, loA), rngB = __fsub_rn(hiB, loB);
+    const float MA = fmaxf(fabsf(loA), fabsf(hiA)), MB = fmaxf(fabsf(loB), fabsf(hiB));
+    const bool okA = rngA >= 1e-30f && rngA <= 1e30f && MA <= 1e30f;
+    const bool okB = rngB >= 1e-30f && rngB <= 1e30f && MB <= 1e30f;
+    const float invA = okA ? __fdividef((float)L, rngA) : 0.f;
+    const float invB = okB ? __fdividef((float)L, rngB) : 0.f;
+    const float sA = __fmul_rn(rngA, 1.0f / (float)L), sB = __fmul_rn(rngB, 1.0f / (float)L);
+    float sseA = 0.f, sseB = 0.f, rmA = 0.f, rmB = 0.f;
+#pragma unroll
+    for (int k = 0; k < EPL; k++) {
+        const float cA = fminf(fmaxf(x[k], loA), hiA);
+        const float cB = fminf(fmaxf(x[k], loB), hiB);
+        const float vA = __fmul_rn(__fsub_rn(cA, loA), invA);
+        const float vB = __fmul_rn(__fsub_rn(cB, loB), invB);
+        const float qA = rintf(vA), qB = rintf(vB);
+        rmA = fmaxf(rmA, fabsf(__fsub_rn(vA, qA)));
+        rmB = fmaxf(rmB, fabsf(__fsub_rn(vB, qB)));
+        float eA = __fsub_rn(x[k], __fmaf_rn(qA, sA, loA));
+        float eB = __fsub_rn(x[k], __fmaf_rn(qB, sB, loB));
+        if (PAD) {
+            const bool in = Lay::elem(lig, k) < d;
+            eA = in ? eA : 0.f;
+            eB = in ? eB : 0.f;
+        }
+        sseA = __fmaf_rn(eA, eA, sseA);
+        sseB = __fmaf_rn(eB, eB, sseB);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        sseA += __shfl_xor_sync(DS_FULL_MASK, sseA, o, G);
+        sseB += __shfl_xor_sync(DS_FULL_MASK, sseB, o, G);
+        rmA = fmaxf(rmA, __shfl_xor_sync(DS_FULL_MASK, rmA, o, G));
+        rmB = fmaxf(rmB, __shfl_xor_sync(DS_FULL_MASK, rmB, o, G));
+    }
+    SA = sseA;
+    SB = sseB;
+    const float fd = (float)d;
+    const float epsw = 10.f * kU * (float)L;  // |v_fast - v_ref|
+    auto bound = [&](float S, float M, float s32, float rmax, bool ok) -> float {
+        if (!ok) return INFINITY;
+        const float delta = 16.f * kU * M + 1e-44f;  // |deq_fast - deq_ref|
+        float b = 2.f * delta * sqrtf(fd * S) + 2.f * fd * delta * delta +
+                  (float)(EPL + log2i<G>() + 4) * kU * S;
+        if (rmax > 0.5f - epsw) b += fd * 4.f * s32 * (epsw * s32 + 2.f * delta);  // code ties
+        return 1.5f * b + 1e-37f;
+    };
+    BA = bound(SA, MA, sA, rmA, okA);
+    BB = bound(SB, MB, sB, rmB, okB);
+}
+
 // ---------------------------------------------------------------------------
 // greedy range search of one row per group (quant.py:160-209), certified.
 // All lanes of the warp must call it (exact re-evaluation is warp-collective).
@@ -399,8 +458,7 @@ __device__ __forceinline__ void greedy_row(const float (&x)[C * VEC], int d, int
         b.hi = __double2float_rn(__dsub_rn(cur_hi, step));
         a.has_me = b.has_me = false;
         a.me = b.me = 0.0;
-        eval_fast<G, C, VEC, PAD>(x, d, lig, a.lo, a.hi, L, a.S, a.B);
-        eval_fast<G, C, VEC, PAD>(x, d, lig, b.lo, b.hi, L, b.S, b.B);
+        eval_fast2<G, C, VEC, PAD>(x, d, lig, a.lo, a.hi, b.lo, b.hi, L, a.S, a.B, b.S, b.B);
         // take_a = me_a <= me_b (quant.py:198)
         bool take_a = true;
         bool sure = true;

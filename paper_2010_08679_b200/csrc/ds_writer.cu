@@ -12,12 +12,13 @@ struct WarpPlan {
     int tr, threads;
     size_t smem;
 };
-static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c) {
+static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c, int mode = 1) {
     const int rpc = 32 / c.G;
     const int ns = c.G == 1 ? 2 : DS_WRITER_NS;  // writer_stages<G>()
     auto warp_bytes = [&](int trr) {
         return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) +
-               (size_t)ns * ((rpc * d * 4 + 63) & ~63);
+               (size_t)ns * ((rpc * d * 4 + 63) & ~63) +
+               (mode == 2 ? (size_t)align16(rpc * (d + 8) * 8) : 0);
     };
     WarpPlan p;
     p.tr = 32;
@@ -34,8 +35,10 @@ static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
     int tr = 32;
     for (int v = 0; v < 2; v++) {  // float4 or scalar layout, whichever the call picks
         if (v == 1 && dim % 4) continue;
-        const WarpPlan p = warp_plan((int)dim, 8 + 8 * dim, pick_cfg((int)dim, v == 1, 1));
-        tr = p.tr < tr ? p.tr : tr;
+        for (int m = 1; m <= 2; m++) {
+            const WarpPlan p = warp_plan((int)dim, 8 + 8 * dim, pick_cfg((int)dim, v == 1, m), m);
+            tr = p.tr < tr ? p.tr : tr;
+        }
     }
     return rows / tr + ntables + 1;
 }
@@ -135,11 +138,11 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     int tr;
     int threads = WT;
     size_t smem;
-    if (mode != 2) {
+    if (mode != 2 || !DS_GREEDY_CTA) {
         // warp pipeline: tiles of 32 records, per-warp record stage + codes
-        // scratch + a ring of NS row chunks of 32/G rows (writer_warp_kernel
-        // computes the same layout)
-        const WarpPlan wp = warp_plan(d, a.rec, c);
+        // scratch + a ring of NS row chunks of 32/G rows (+ the greedy exact
+        // scratch; writer_warp_kernel computes the same layout)
+        const WarpPlan wp = warp_plan(d, a.rec, c, mode);
         tr = wp.tr;
         threads = wp.threads;
         smem = wp.smem;
@@ -158,7 +161,7 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         // incremental counts live on the device; bound by table rows
         max_tiles += (tables_host[t].rows + tr - 1) / tr;
     }
-    if (mode != 2) max_tiles = (max_tiles + threads / 32 - 1) / (threads / 32);  // warps -> CTAs
+    if (mode != 2 || !DS_GREEDY_CTA) max_tiles = (max_tiles + threads / 32 - 1) / (threads / 32);  // warps -> CTAs
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     int per_sm = 0;

@@ -611,8 +611,12 @@ __device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
 template <int G>
 __host__ __device__ constexpr int writer_stages() { return G == 1 ? 2 : DS_WRITER_NS; }
 
+#ifndef DS_WRITER_MINB_GREEDY
+#define DS_WRITER_MINB_GREEDY 2
+#endif
 template <int G, int C, int VEC, int MODE, bool PAD>
-__global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const WriterArgs a) {
+__global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
+    writer_warp_kernel(const WriterArgs a) {
     constexpr int EPL = C * VEC;
     constexpr int RPC = 32 / G;  // rows per chunk
     constexpr int NS = writer_stages<G>();
@@ -627,12 +631,14 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
     const int stage_b = align16(TR * a.rec) + 16;
     const int codes_b = align16(RPC * d);
     const int chunk_b = (RPC * d * 4 + 63) & ~63;  // whole 4-chunk swizzle groups
-    const int warp_b = stage_b + codes_b + NS * chunk_b;
+    const int exact_b = MODE == 2 ? align16(RPC * (d + 8) * 8) : 0;  // greedy exact scratch
+    const int warp_b = stage_b + codes_b + NS * chunk_b + exact_b;
     uint8_t *smem_al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 15) & ~(uintptr_t)15);
     uint8_t *wbase = smem_al + (size_t)wid * warp_b;
     uint8_t *stage = wbase;
     uint8_t *codes = wbase + stage_b;
     float *ring = reinterpret_cast<float *>(codes + codes_b);
+    double *exact = reinterpret_cast<double *>(codes + codes_b + NS * chunk_b);
     // 16-byte chunk g of a stage: swizzled when each lane reads its own row
     // (G == 1: rows 64 B apart would put 4 lanes on one bank group), natural
     // otherwise (consecutive lanes already read consecutive chunks, and the
@@ -750,7 +756,7 @@ __global__ void __launch_bounds__(WT, DS_WRITER_MINB) writer_warp_kernel(const W
                 }
                 const bool fix = code_row<G, C, VEC, MODE, PAD, VEC == 4 && G == 1>(a, td, x, row, valid, valid ? loc : 0,
                                                                 stage + r * a.rec, codes + slot * d,
-                                                                nullptr, lig, d, acc);
+                                                                exact + slot * (d + 8), lig, d, acc);
                 if (MODE == 1) {  // record r's flag to lane r
                     const bool f = __shfl_sync(DS_FULL_MASK, fix, ((lane - sub * RPC) & (RPC - 1)) * G);
                     if (lane >= sub * RPC && lane < (sub + 1) * RPC) row_fix |= f;
@@ -860,6 +866,9 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
 // host dispatch
 // ---------------------------------------------------------------------------
 typedef void (*writer_fn)(const WriterArgs);
+#ifndef DS_GREEDY_CTA
+#define DS_GREEDY_CTA 0  // 1: the greedy ranges run in the CTA-tiled writer_kernel
+#endif
 
 struct Cfg {
     int G, C, VEC;
@@ -902,7 +911,7 @@ static writer_fn select_writer(const Cfg &c) {
 #define DS_W(G_, C_, V_) \
     if (c.G == G_ && c.C == C_ && c.VEC == V_)                                                  \
     {                                                                                            \
-        if constexpr (MODE == 2) return writer_kernel<G_, C_, V_, MODE, PAD>;                    \
+        if constexpr (MODE == 2 && DS_GREEDY_CTA) return writer_kernel<G_, C_, V_, MODE, PAD>;   \
         else return writer_warp_kernel<G_, C_, V_, MODE, PAD>;                                   \
     }
     DS_W(1, 1, 4) DS_W(1, 2, 4) DS_W(1, 4, 4) DS_W(2, 4, 4) DS_W(4, 4, 4) DS_W(8, 4, 4)
