@@ -61,6 +61,11 @@ WORKLOADS = {
                             "(bins 45, ratio 0.2)",
                        cards=[125_000_000], dim=128, bitwidth=4, adaptive=True, lookups="uniform",
                        n_per_table=37_500_000),
+    # configs[4]: restore of a full checkpoint + 5 incremental deltas
+    "C5": dict(desc="C5: restore a chain (1 full + 5 incremental 8-bit checkpoints of the C2 "
+                    "tables) into device tables: unpack, dequantize, scatter, baseline bits",
+               cards=CRITEO_KAGGLE, dim=16, bitwidth=8, adaptive=False, lookups="zipf",
+               n_per_table=BATCHES * BATCH, restore=5),
     # configs[2], one of 8 GPU shards: Criteo-TB rows / 8, 4-bit adaptive greedy
     "C3": dict(desc="C3 (one of 8 GPU shards): Criteo-TB-shaped 26 tables / 8 x dim 128 fp32, "
                     "4-bit adaptive greedy (bins 45, ratio 0.2), 500 x 2048 Zipf lookups/table",
@@ -510,10 +515,123 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_restore(args):
+    """C5: restore a 1 full + 5 incremental chain through the public API
+    (engine.apply_payload, i.e. ds_restore_section per section).
+
+    value: restored fp32 row bytes (all records of the chain x 4*dim) / device
+    time of the chain with the payloads resident in HBM; e2e: the same with
+    the payload bytes H2D-copied from pinned host memory inside the timed
+    region.  Single GPU (a row-sharded restore runs the same kernels on each
+    rank's row range).
+    """
+    import torch
+    import paper_2010_08679_b200 as ds
+    from paper_2010_08679_b200.engine import ShardWriter, apply_payload
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    from paper_2010_08679_b200.tracker import ModelTracker
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w = workload_of(args)
+    cards, dim = w["cards"], w["dim"]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(args.seed * 7919)
+    tables = [ds.DeviceTable(t, torch.rand((r, dim), generator=gen, device=dev).mul_(2).sub_(1))
+              for t, r in enumerate(cards)]
+    # the chain: a full checkpoint, then 5 intervals of Zipf lookups
+    chain = []
+    full = ShardWriter(tables, w["bitwidth"], adaptive=None, device=dev)
+    buf = torch.empty(full.payload_bytes(None) + 16, dtype=torch.uint8, device=dev)
+    full.write(buf)
+    n, _ = full.finish()
+    chain.append(("full", buf[:n].clone()))
+    ck = ShardedCheckpointer(tables, w["bitwidth"], adaptive_overrides={w["bitwidth"]: None},
+                             device=dev)
+    for k in range(w["restore"]):
+        lk = [lookups_torch(w["lookups"], r, w["n_per_table"], gen, dev) for r in cards]
+        ck.step(pack_lookups_device(lk, cards, dev))
+        nb = int(ck.writer.sec_off[-1].item())
+        chain.append(("incremental", ck.payload[:nb].clone()))
+        for t in tables:  # the training step between checkpoints
+            t.values.add_(0.01)
+    host = [(kind, b.cpu().numpy().tobytes()) for kind, b in chain]
+    pinned = [torch.from_numpy(np.frombuffer(h, np.uint8).copy()).pin_memory() for _, h in host]
+    from paper_2010_08679_b200.payload import parse_headers
+    rows_restored = sum(i.rows for (kind, h) in host for i in parse_headers(h, kind != "full"))
+    out = {t.table_id: ds.DeviceTable(t.table_id, torch.zeros_like(t.values)) for t in tables}
+    tr = ModelTracker({t.table_id: t.rows for t in tables}, device=dev)
+    base = {tid: tr.baseline_bitmap(tid) for tid in out}
+    dbufs = [torch.cat([b, torch.zeros(16, dtype=torch.uint8, device=dev)]) for _, b in chain]
+
+    def restore_once(from_host):
+        checks = []
+        for (kind, h), db, pin in zip(host, dbufs, pinned):
+            if from_host:
+                db[:pin.numel()].copy_(pin, non_blocking=True)
+            checks.append(apply_payload(h, kind != "full", out, base if kind != "full" else None,
+                                        device=dev, device_buf=db, sync=False))
+        return checks
+
+    for _ in range(max(3, args.warmup)):
+        for c in restore_once(False):
+            c()
+    torch.cuda.synchronize()
+    K = args.steps
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    times, times_e2e = [], []
+    with ClockSampler(0) as clocks:
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            checks = restore_once(False)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            for c in checks:
+                c()
+        for k in range(K):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            checks = restore_once(True)
+            for c in checks:
+                c()
+            torch.cuda.synchronize()
+            times_e2e.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    te = float(np.mean(times_e2e))
+    nbytes = rows_restored * dim * 4
+    h2d = sum(p.numel() for p in pinned)
+    # roofline: the restore kernels' algorithmic bytes = chain bytes read +
+    # restored fp32 rows written
+    alg = h2d + nbytes
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    line = {
+        "metric": "restored GB/s of embedding rows (unpack+dequantize+scatter)", "value": nbytes / t / 1e9,
+        "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32 via f64",
+        "data": "synthetic", "config": dict(workload_desc(w), chain_records=rows_restored,
+                                            chain_bytes=h2d),
+        "roofline": {"bound": "hbm", "kernel": "ds::restore_kernel (all sections of the chain)",
+                     "achieved": alg / t / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": alg / t / 1e9 / peak, "traffic": None},
+        "e2e": {"value": nbytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4 * len(host) * 26},
+        "clocks": clocks.summary(), "gpu_launches": K * sum(1 for (kind, h) in host
+                                                         for _ in parse_headers(h, kind != "full")),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif WORKLOADS[args.workload].get("restore"):
+        run_restore(args)
     else:
         run_ours(args)
 

@@ -256,7 +256,7 @@ def _upload_payload(data, dev) -> torch.Tensor:
 
 
 def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None = None,
-                  device=None) -> None:
+                  device=None, device_buf: torch.Tensor | None = None, sync: bool = True):
     """Apply one shard payload to device tables (the loop body of
     engine.py:625-649).
 
@@ -265,13 +265,16 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
     of the since-baseline scope rebuilt for incremental sections (:476).
     Errors are raised in the reference's order: the first failing section
     wins; within a section FormatError precedes IntegrityError.
+    device_buf: the same bytes already in device memory (no upload);
+    sync=False: launch only and return a callable that checks the flags later
+    (restore pipelines check once per chain).
     """
     dev = device_of(device)
     infos = parse_headers(data, incremental)  # FormatError for any bad header
     if not infos:
-        return
+        return (lambda: None) if not sync else None
     L = _lib.lib()
-    buf = _upload_payload(data, dev)
+    buf = device_buf if device_buf is not None else _upload_payload(data, dev)
     flags = torch.zeros(len(infos), dtype=torch.int32, device=dev)
     host_err = None
     stream = _lib.stream_handle()
@@ -296,12 +299,17 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
             t.values.data_ptr(), t.values.stride(0), aux_ptr,
             None if bm is None else bm.words.data_ptr(), flags[k:].data_ptr(), stream),
             "restore_section")
-    fl = flags.cpu().numpy()
-    first_dev = next((k for k in range(len(infos)) if fl[k]), None)
-    if first_dev is not None and (host_err is None or first_dev < host_err[0]):
-        _lib.raise_flags(int(fl[first_dev]), f"restore (table {infos[first_dev].table_id})")
-    if host_err is not None:
-        raise host_err[1]
+    def check():
+        fl = flags.cpu().numpy()
+        first_dev = next((k for k in range(len(infos)) if fl[k]), None)
+        if first_dev is not None and (host_err is None or first_dev < host_err[0]):
+            _lib.raise_flags(int(fl[first_dev]), f"restore (table {infos[first_dev].table_id})")
+        if host_err is not None:
+            raise host_err[1]
+
+    if not sync:
+        return check
+    check()
 
 
 @dataclass
