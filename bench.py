@@ -445,7 +445,7 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(args.workload, {}).get(dom)
-    wk = ("ds::writer_kernel (adaptive greedy, compute-bound)" if w["adaptive"]
+    wk = ("ds::writer_warp_kernel (adaptive greedy ranges, compute-bound)" if w["adaptive"]
           else "ds::writer_warp_kernel (naive ranges)")
     roofline = {"bound": "hbm", "kernel": {"mark": "ds::mark_tma_kernel", "write": wk}[dom],
                 "measured_over": {"mark": "the mark phase (one mark_tma launch per step)",
@@ -455,6 +455,18 @@ def run_ours(args):
                 "achieved": phases[dom]["GB/s"], "peak": peak, "unit": "GB/s",
                 "frac": phases[dom]["GB/s"] / peak, "traffic": traffic,
                 "peak_source": peak_src}
+    if w["adaptive"] and dom == "write":
+        # the greedy search is compute-bound: SURVEY 8(d)'s op count per row,
+        # 13*d*(E+1) + 2d with E = 2*steps + 1 candidate evaluations, against
+        # the fp32 lane-op rate (SMs x 128 x max SM clock)
+        bins, ratio = {2: (25, 0.5), 3: (25, 0.2), 4: (45, 0.2)}[w["bitwidth"]]
+        E = 2 * int(np.floor(bins * ratio + 1e-9)) + 1
+        ops = dirty_rank * (13 * DIM * (E + 1) + 2 * DIM)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_ops = sms * 128 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        roofline["compute"] = {"unit": "Gop/s", "ops_per_step": ops, "achieved": ops / t_write / 1e9,
+                               "peak": peak_ops / 1e9, "frac": ops / t_write / peak_ops,
+                               "evaluations_per_row": E}
 
     # ---- e2e through the public API with host buffers --------------------------------
     # The public pipeline API (paper_2010_08679_b200.pipeline): each step's
