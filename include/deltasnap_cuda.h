@@ -214,6 +214,26 @@ DS_API int ds_restore_section(const uint8_t *body, int64_t nrec, int64_t dim, in
                        float *values, int64_t ld, float *aux_values, uint32_t *baseline_words,
                        uint32_t *flags, void *stream);
 
+/* One section of a payload for ds_restore_payload. */
+typedef struct {
+    int64_t body_off;      /* byte offset of the section's first record in `payload` */
+    int64_t nrec;          /* records in the section (row_count) */
+    float *values;         /* the (local) table: rows [row_lo, row_hi) of table_rows */
+    float *aux_values;     /* may be NULL */
+    uint32_t *baseline;    /* since-baseline words of the table (may be NULL) */
+    int64_t ld;            /* row stride of values / aux_values (floats) */
+    int64_t table_rows;    /* global rows of the table */
+    int64_t row_lo, row_hi;
+} ds_restore_sec;
+
+/* Every section of one payload in ONE launch (same semantics as
+ * ds_restore_section per section).  Sections share dim, bitwidth, aux and
+ * kind; flags[k] receives section k's DS_FLAG_* bits (so the host raises the
+ * first failing section's error, engine.py:459-472).  At most 64 sections. */
+DS_API int ds_restore_payload(const uint8_t *payload, const ds_restore_sec *secs_host, int nsec,
+                              int64_t dim, int bitwidth, int aux, int incremental, uint32_t *flags,
+                              void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Row-matrix codec entry points (quant.py API mirror)                  */
 /* ------------------------------------------------------------------ */

@@ -69,6 +69,20 @@ class CkptParams(ctypes.Structure):
     ]
 
 
+class RestoreSec(ctypes.Structure):
+    _fields_ = [
+        ("body_off", ctypes.c_int64),
+        ("nrec", ctypes.c_int64),
+        ("values", ctypes.c_void_p),
+        ("aux_values", ctypes.c_void_p),
+        ("baseline", ctypes.c_void_p),
+        ("ld", ctypes.c_int64),
+        ("table_rows", ctypes.c_int64),
+        ("row_lo", ctypes.c_int64),
+        ("row_hi", ctypes.c_int64),
+    ]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
@@ -93,6 +107,7 @@ _SIGNATURES = {
     "ds_record_size": (_I64, [_I64, _I, _I, _I]),
     "ds_restore_section": (_I, [_P, _I64, _I64, _I, _I, _I, _I64, _I64, _I64, _P, _I64, _P, _P,
                                 _P, _P]),
+    "ds_restore_payload": (_I, [_P, _P, _I, _I64, _I, _I, _I, _P, _P]),
     "ds_quantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),
     "ds_dequantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P, _P]),
     "ds_reconstruction_errors": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),

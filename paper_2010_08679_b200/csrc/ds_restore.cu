@@ -127,6 +127,108 @@ __global__ void __launch_bounds__(RT) restore_kernel(const RestoreArgs a) {
     if (bad_row) atomicOr(a.flags, DS_FLAG_INTEGRITY);
 }
 
+// ---------------------------------------------------------------------------
+// Every section of a payload in one launch: tiles of records across sections,
+// staged into shared memory with aligned 32-bit loads; G lanes per record,
+// each lane 4 consecutive elements at a time (one 32-bit code read, 4 exact
+// dequantizations, one 16-byte store when the table rows allow it).
+// ---------------------------------------------------------------------------
+struct RestorePArgs {
+    const uint8_t *payload;
+    ds_restore_sec s[DS_MAX_TABLES];
+    int64_t rec_begin[DS_MAX_TABLES], rec_end[DS_MAX_TABLES];
+    int64_t tile_off[DS_MAX_TABLES + 1];
+    uint32_t *flags;
+    int nsec, dim, bitwidth, L, aux, incremental, rec, par_off, code_off, packed, aux_off;
+    int tile_rows, vec;
+    double invL;
+};
+
+__device__ __forceinline__ uint32_t lds32u(const uint8_t *base, int o) {
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(base + (o & ~3));
+    const int sh = (o & 3) * 8;
+    return sh ? __funnelshift_r(w[0], w[1], sh) : w[0];
+}
+
+template <int G>
+__global__ void __launch_bounds__(RT) restore_payload_kernel(const RestorePArgs a) {
+    extern __shared__ __align__(16) uint8_t stage[];
+    constexpr int RPP = RT / G;
+    const int lane = threadIdx.x & 31, lig = lane & (G - 1), slot = threadIdx.x / G;
+    const int d = a.dim, TR = a.tile_rows, N = a.bitwidth;
+    const int64_t ntiles = a.tile_off[a.nsec];
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int sec = 0;  // last section whose first tile <= tile (binary search, uniform)
+        for (int lo = 0, hi = a.nsec - 1; lo <= hi;) {
+            const int mid = (lo + hi) >> 1;
+            if (a.tile_off[mid] <= tile) { sec = mid; lo = mid + 1; }
+            else hi = mid - 1;
+        }
+        const ds_restore_sec &S = a.s[sec];
+        const int64_t r0 = a.rec_begin[sec] + (tile - a.tile_off[sec]) * TR;
+        const int nr = (int)min((int64_t)TR, a.rec_end[sec] - r0);
+        const uint8_t *src = a.payload + S.body_off + r0 * a.rec;
+        const int nw = (nr * a.rec + 3) >> 2;
+        // the last word may read up to 3 bytes past the run: the host keeps
+        // 16 bytes of slack after every staged payload
+        for (int k = threadIdx.x; k < nw; k += RT)
+            reinterpret_cast<uint32_t *>(stage)[k] = ld4_unaligned_g(src + 4 * k);
+        __syncthreads();
+        bool bad_fmt = false, bad_row = false;
+        for (int p = 0; p < nr; p += RPP) {
+            const int r = p + slot;
+            if (r >= nr) continue;
+            const int ro = r * a.rec;
+            int64_t gid = r0 + r;
+            if (a.incremental) {
+                gid = (int64_t)(((uint64_t)lds32u(stage, ro + 4) << 32) | lds32u(stage, ro));
+                if (gid < 0 || gid >= S.table_rows) {  // engine.py:470-472
+                    bad_row = true;
+                    continue;
+                }
+            }
+            if (gid < S.row_lo || gid >= S.row_hi) continue;  // another rank's rows
+            const int64_t local = gid - S.row_lo;
+            float *dst = S.values + local * S.ld;
+            if (N == 0) {
+                for (int e = lig; e < d; e += G) dst[e] = __uint_as_float(lds32u(stage, ro + a.par_off + 4 * e));
+            } else {
+                const float lo = __uint_as_float(lds32u(stage, ro + a.par_off));
+                const float hi = __uint_as_float(lds32u(stage, ro + a.par_off + 4));
+                const double s = scale64_y(lo, hi, (double)a.L, a.invL);
+                for (int m = lig; 4 * m < d; m += G) {
+                    const int bit = 4 * m * N;
+                    const uint32_t w = lds32u(stage, ro + a.code_off + (bit >> 3)) >> (bit & 7);
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) v[j] = deq_exact((int)((w >> (j * N)) & (uint32_t)a.L), lo, s);
+                    if (a.vec && 4 * m + 4 <= d)
+                        *reinterpret_cast<float4 *>(dst + 4 * m) = make_float4(v[0], v[1], v[2], v[3]);
+                    else
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            if (4 * m + j < d) dst[4 * m + j] = v[j];
+                }
+                // padding bits must be zero (quant.py:390-392)
+                if (lig == 0) {
+                    const int padbits = 8 * a.packed - d * N;
+                    if (padbits > 0 && (stage[ro + a.code_off + a.packed - 1] >> (8 - padbits)) != 0)
+                        bad_fmt = true;
+                }
+            }
+            if (a.aux && S.aux_values) {
+                float *adst = S.aux_values + local * S.ld;
+                for (int e = lig; e < d; e += G) adst[e] = __uint_as_float(lds32u(stage, ro + a.aux_off + 4 * e));
+            }
+            if (a.incremental && S.baseline && lig == 0)  // mark_baseline, engine.py:476
+                atomicOr(S.baseline + (local >> 5), 1u << (local & 31));
+        }
+        if (bad_fmt) atomicOr(a.flags + sec, DS_FLAG_FORMAT);
+        if (bad_row) atomicOr(a.flags + sec, DS_FLAG_INTEGRITY);
+        __syncthreads();
+    }
+}
+
 }  // namespace ds
 
 using namespace ds;
@@ -195,4 +297,76 @@ extern "C" int ds_restore_section(const uint8_t *body, int64_t nrec, int64_t dim
     if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     fn<<<(unsigned)grid, RT, smem, s>>>(a);
     return host::check_launch("ds_restore_section");
+}
+
+extern "C" int ds_restore_payload(const uint8_t *payload, const ds_restore_sec *secs, int nsec,
+                                  int64_t dim, int bitwidth, int aux, int incremental,
+                                  uint32_t *flags, void *stream) {
+    if (!(bitwidth == 0 || bitwidth == 2 || bitwidth == 3 || bitwidth == 4 || bitwidth == 8))
+        return host::fail(DS_ERR_FORMAT, "ds_restore_payload: invalid bitwidth");
+    if (nsec < 1 || nsec > DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_restore_payload: nsec (1..64)");
+    if (dim < 1 || dim > 65536) return host::fail(DS_ERR_ARG, "ds_restore_payload: dim");
+    if (!payload || !secs || !flags) return host::fail(DS_ERR_ARG, "ds_restore_payload: null pointer");
+    RestorePArgs a;
+    a.payload = payload;
+    a.flags = flags;
+    a.nsec = nsec;
+    a.dim = (int)dim;
+    a.bitwidth = bitwidth;
+    a.L = bitwidth ? (1 << bitwidth) - 1 : 0;
+    a.invL = bitwidth ? 1.0 / (double)a.L : 0.0;
+    a.aux = aux;
+    a.incremental = incremental;
+    a.rec = (int)ds_record_size(dim, bitwidth, aux, incremental);
+    a.par_off = incremental ? 8 : 0;
+    a.code_off = a.par_off + 8;
+    a.packed = bitwidth ? (int)((dim * bitwidth + 7) / 8) : 0;
+    a.aux_off = bitwidth ? a.code_off + a.packed : a.par_off + 4 * (int)dim;
+    // lanes per record: one per 4-element group, up to a warp
+    int G = 1;
+    while (G * 4 < dim && G < 32) G <<= 1;
+    const int rpp = RT / G;
+    int tr = rpp;
+    while (tr * 2 * a.rec <= 32 * 1024 && tr < 1024) tr *= 2;
+    while (tr > rpp && tr * a.rec > 32 * 1024) tr /= 2;
+    a.tile_rows = tr;
+    a.vec = 1;
+    int64_t tiles = 0;
+    for (int k = 0; k < nsec; k++) {
+        a.s[k] = secs[k];
+        if (!secs[k].values) return host::fail(DS_ERR_ARG, "ds_restore_payload: null values");
+        if (secs[k].ld % 4 || reinterpret_cast<uintptr_t>(secs[k].values) % 16) a.vec = 0;
+        int64_t b = 0, e = secs[k].nrec;
+        if (!incremental) {  // record i is row i: visit only this table's rows
+            b = secs[k].row_lo > 0 ? secs[k].row_lo : 0;
+            e = secs[k].row_hi < e ? secs[k].row_hi : e;
+            if (e < b) e = b;
+        }
+        a.rec_begin[k] = b;
+        a.rec_end[k] = e;
+        a.tile_off[k] = tiles;
+        tiles += (e - b + tr - 1) / tr;
+    }
+    a.tile_off[nsec] = tiles;
+    if (tiles == 0) return DS_OK;
+    size_t smem = ((size_t)tr * a.rec + 15) / 16 * 16 + 16;
+    if (smem > 200 * 1024) return host::fail(DS_ERR_CONFIG, "ds_restore_payload: record too large");
+    void (*fn)(const RestorePArgs) = nullptr;
+    switch (G) {
+        case 1: fn = restore_payload_kernel<1>; break;
+        case 2: fn = restore_payload_kernel<2>; break;
+        case 4: fn = restore_payload_kernel<4>; break;
+        case 8: fn = restore_payload_kernel<8>; break;
+        case 16: fn = restore_payload_kernel<16>; break;
+        default: fn = restore_payload_kernel<32>; break;
+    }
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, RT, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t cap = (int64_t)host::sm_count() * per_sm;
+    const int64_t grid = tiles < cap ? tiles : cap;
+    fn<<<(unsigned)grid, RT, smem, (cudaStream_t)stream>>>(a);
+    return host::check_launch("ds_restore_payload");
 }

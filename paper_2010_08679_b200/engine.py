@@ -276,29 +276,49 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
     L = _lib.lib()
     buf = device_buf if device_buf is not None else _upload_payload(data, dev)
     flags = torch.zeros(len(infos), dtype=torch.int32, device=dev)
+    # host-side checks first: sections from the first failing one on are not applied
     host_err = None
-    stream = _lib.stream_handle()
     for k, info in enumerate(infos):
         t = tables.get(info.table_id)
         if t is None:
             host_err = (k, IntegrityError(f"payload names unknown table {info.table_id}"))
-            break
-        if info.dim != t.dim:
+        elif info.dim != t.dim:
             host_err = (k, IntegrityError(f"dim mismatch in table {info.table_id}"))
-            break
-        if not incremental and info.rows != t.total_rows:
+        elif not incremental and info.rows != t.total_rows:
             host_err = (k, IntegrityError(
                 f"full section for table {info.table_id} has {info.rows} rows, "
                 f"expected {t.total_rows}"))
+        if host_err is not None:
             break
-        bm = baseline.get(info.table_id) if (baseline is not None and incremental) else None
-        aux_ptr = t.aux.data_ptr() if (info.aux and t.aux is not None) else None
-        _lib.check(L.ds_restore_section(
-            buf.data_ptr() + info.body_offset, info.rows, info.dim, info.bitwidth or 0,
-            int(info.aux), int(incremental), t.total_rows, t.row_base, t.row_base + t.rows,
-            t.values.data_ptr(), t.values.stride(0), aux_ptr,
-            None if bm is None else bm.words.data_ptr(), flags[k:].data_ptr(), stream),
-            "restore_section")
+    napply = len(infos) if host_err is None else host_err[0]
+    stream = _lib.stream_handle()
+    # one launch per run of sections sharing (dim, bitwidth, aux) -- normally
+    # the whole payload (ds_restore_payload, <= 64 sections per launch)
+    k0 = 0
+    while k0 < napply:
+        key = (infos[k0].dim, infos[k0].bitwidth, infos[k0].aux)
+        k1 = k0
+        while (k1 < napply and k1 - k0 < _lib.MAX_TABLES and
+               (infos[k1].dim, infos[k1].bitwidth, infos[k1].aux) == key):
+            k1 += 1
+        secs = (_lib.RestoreSec * (k1 - k0))()
+        for j, info in enumerate(infos[k0:k1]):
+            t = tables[info.table_id]
+            bm = baseline.get(info.table_id) if (baseline is not None and incremental) else None
+            secs[j].body_off = info.body_offset
+            secs[j].nrec = info.rows
+            secs[j].values = t.values.data_ptr()
+            secs[j].aux_values = t.aux.data_ptr() if (info.aux and t.aux is not None) else None
+            secs[j].baseline = None if bm is None else bm.words.data_ptr()
+            secs[j].ld = t.values.stride(0)
+            secs[j].table_rows = t.total_rows
+            secs[j].row_lo = t.row_base
+            secs[j].row_hi = t.row_base + t.rows
+        _lib.check(L.ds_restore_payload(
+            buf.data_ptr(), ctypes.cast(secs, ctypes.c_void_p), k1 - k0, key[0], key[1] or 0,
+            int(key[2]), int(incremental), flags[k0:].data_ptr(), stream), "restore_payload")
+        k0 = k1
+
     def check():
         fl = flags.cpu().numpy()
         first_dev = next((k for k in range(len(infos)) if fl[k]), None)
