@@ -106,7 +106,7 @@ def workload_desc(w):
         "tables": len(w["cards"]), "rows_per_rank": int(sum(w["cards"])), "dim": w["dim"],
         "bitwidth": w["bitwidth"], "ranges": "adaptive greedy" if w["adaptive"] else "naive min/max",
         "lookups": w["lookups"], "lookups_per_step_per_rank": int(w["n_per_table"] * len(w["cards"])),
-        "lookup_dtype": "per table: u8 (<=256 rows), u16 (<=65536), i32 (above)",
+        "lookup_dtype": "per table: ids bit-packed at ceil(log2(rows)) bits (LookupStream)",
         "scope": "interval (consecutive increments)",
         "row_map": "Zipf rank -> row through a seeded permutation per table"
                    if w["lookups"] == "zipf" else "uniform row ids",
@@ -286,18 +286,14 @@ def cpu_measure(w, tables, lookups, budget_s=20.0, steps=None):
             "kind": "port", "sample": sample, "seconds": secs, "steps": reps}
 
 
-def pack_lookups_device(lookups, cards, dev):
-    """Device LookupStream of per-table id tensors at each table's narrowest width."""
-    import torch
+def pack_lookups(lookups, cards, dev):
+    """The interval's lookup stream through the public API: each table's ids
+    bit-packed at ceil(log2(rows)) bits (LookupStream.pack, pinned host
+    memory), and its device copy."""
     from paper_2010_08679_b200.tracker import LookupStream
-    boff, cnt, wid, tids, total = LookupStream.layout(dict(enumerate(cards)),
-                                                      {t: lk.numel() for t, lk in enumerate(lookups)})
-    buf = torch.zeros(max(16, total), dtype=torch.uint8, device=dev)
-    for t, (o, n, w) in enumerate(zip(boff, cnt, wid)):
-        x = lookups[t].to(torch.int64)
-        parts = [((x >> (8 * k)) & 0xFF).to(torch.uint8) for k in range(w)]
-        buf[o:o + n * w] = torch.stack(parts, dim=1).reshape(-1)
-    return LookupStream(buf, boff, cnt, wid, tids)
+    host = LookupStream.pack({t: lk.cpu().numpy() for t, lk in enumerate(lookups)},
+                             dict(enumerate(cards)), pin=True)
+    return host, host.to(dev, non_blocking=False)
 
 
 # --------------------------------------------------------------------------------
@@ -356,9 +352,9 @@ def run_ours(args):
         v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
         tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
     lookups = [lookups_torch(w["lookups"], r, n_look, gen, dev) for r in cards]
-    # the interval's lookup stream, each table at its narrowest id width
-    # (u8 <= 256 rows, u16 <= 65536, i32 above): ds_mark_packed's input
-    stream = pack_lookups_device(lookups, cards, dev)
+    # the interval's lookup stream, each table's ids at ceil(log2(rows))
+    # bits: ds_mark_packed's input (host copy for e2e, device copy in HBM)
+    host_stream, stream = pack_lookups(lookups, cards, dev)
     # ranges: the reference's default for the bitwidth (engine.py:112-115),
     # or naive min/max when the workload says so
     overrides = None if w["adaptive"] else {w["bitwidth"]: None}
@@ -477,8 +473,6 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         from paper_2010_08679_b200.pipeline import CheckpointPipeline
-        host_stream = LookupStream(stream.buf.cpu().pin_memory(), stream.seg_byte_off,
-                                   stream.seg_count, stream.seg_width, stream.seg_tables)
         pipe = CheckpointPipeline(ck, host_stream.nbytes, torch.uint8)
         for _ in range(3):
             pipe.submit(host_stream)
@@ -562,7 +556,7 @@ def run_restore(args):
                              device=dev)
     for k in range(w["restore"]):
         lk = [lookups_torch(w["lookups"], r, w["n_per_table"], gen, dev) for r in cards]
-        ck.step(pack_lookups_device(lk, cards, dev))
+        ck.step(pack_lookups(lk, cards, dev)[1])
         nb = int(ck.writer.sec_off[-1].item())
         chain.append(("incremental", ck.payload[:nb].clone()))
         for t in tables:  # the training step between checkpoints

@@ -92,12 +92,14 @@ DS_API int ds_mark_i32(uint32_t *words, const int64_t *word_off_host, const int6
                        const int32_t *seg_table_host, int nseg, uint32_t *flags, void *stream);
 
 /* Packed mixed-width lookup stream: segment s holds seg_count[s] ids of
- * seg_width[s] bytes (1 and 2: unsigned; 4 and 8: signed two's complement)
- * starting at byte seg_byte_off[s] of `lookups` (16-byte aligned, as is
- * `lookups`), all marking table seg_table[s].  Sending each table's ids at
- * the narrowest width its row count allows (u8 <= 256 rows, u16 <= 65536)
- * cuts the lookup bytes the end-to-end path moves over PCIe and K1 streams
- * from HBM.  Same bit semantics and DS_FLAG_BOUNDS behaviour as ds_mark. */
+ * seg_width[s] BITS starting at byte seg_byte_off[s] of `lookups` (16-byte
+ * aligned, as is `lookups`), all marking table seg_table[s].  Widths 4, 8,
+ * ..., 28: unsigned ids in an LSB-first bitstream (8 and 16 are plain u8 /
+ * u16 arrays); 32 and 64: signed two's-complement int32 / int64.  Each packed
+ * segment must be readable up to the next 16-byte boundary.  Sending each
+ * table's ids at ceil(log2(rows)) bits (rounded up to a multiple of 4) cuts
+ * the lookup bytes the end-to-end path moves over PCIe and K1 streams from
+ * HBM.  Same bit semantics and DS_FLAG_BOUNDS behaviour as ds_mark. */
 DS_API int ds_mark_packed(uint32_t *words, const int64_t *word_off_host, const int64_t *rows_host,
                           const void *lookups, const int64_t *seg_byte_off_host,
                           const int64_t *seg_count_host, const int32_t *seg_width_host,

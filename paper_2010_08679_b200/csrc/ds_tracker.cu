@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ds_common.cuh"
 #include "ds_host.h"
 
@@ -31,7 +33,7 @@ struct MarkArgs {
     const uint8_t *ibytes;             // TMA kernel: packed lookup stream
     int64_t seg_boff[DS_MAX_TABLES];   // TMA kernel: byte offset of each segment (16-aligned)
     int64_t seg_n[DS_MAX_TABLES];      // TMA kernel: ids in each segment
-    int32_t seg_width[DS_MAX_TABLES];  // TMA kernel: bytes per id (1, 2 unsigned; 4, 8 signed)
+    int32_t seg_width[DS_MAX_TABLES];  // TMA kernel: bits per id (4..28 packed, 8/16 unsigned; 32/64 signed)
     int nseg;
 };
 
@@ -166,7 +168,10 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_kernel(const MarkArgs a, in
 // bit.  Correct for any interleaving: bits are only ever set, and a cache
 // entry only claims bits this CTA has itself OR-ed (or seen OR-ed) into HBM.
 // ---------------------------------------------------------------------------
-constexpr int MK_CACHE_BITS = 11;      // 2048 entries (16 KB)
+#ifndef DS_MK_CACHE_BITS
+#define DS_MK_CACHE_BITS 13
+#endif
+constexpr int MK_CACHE_BITS = DS_MK_CACHE_BITS;  // 2^13 entries = 64 KB (A/B: DS_MK_CACHE_BITS)
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -201,31 +206,43 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
 
 // Every CTA works inside ONE segment (one table's slice of the lookup
 // stream) and each of its warps runs its own TMA ring over every 8th chunk of
-// the CTA's range (no CTA barrier in the loop).  Per table size:
-//  * rows <= MK_BYTE_ROWS (all 18 small Criteo-Kaggle tables): a shared
-//    byte per row; a lookup is one plain byte store (racing stores all write
-//    1, so no atomics and no read), folded into bitmap words and OR-ed into HBM
-//    once per CTA at the end;
-//  * rows <= 32 * MK_WIN_WORDS: a shared copy of the bitmap words
+// the CTA's range (no CTA barrier in the loop).  Per table size, in a 64 KB
+// shared region:
+//  * rows <= MK_BYTE_ROWS (65,504; all 18 small Criteo-Kaggle tables): a
+//    shared byte per row; a lookup is one plain byte store (racing stores all
+//    write 1, so no atomics and no read), folded into bitmap words and OR-ed
+//    into HBM once per CTA at the end;
+//  * rows <= 32 * MK_WIN_WORDS (524,288): a shared copy of the bitmap words
 //    (read-before-ATOMS: hot words are already set and same-address reads
 //    broadcast), flushed with one RED per touched word;
 //  * larger: a shared cache of (word, bits known set) with second-chance
-//    replacement; a miss issues one fire-and-forget RED.OR.
+//    replacement (8,192 entries); a miss issues one fire-and-forget RED.OR.
 // Correct for any interleaving: bits are only ever set, and a cache entry
 // only claims bits this CTA itself OR-ed into HBM.
-constexpr int MK_WIN_WORDS = 2048;   // 65536 rows
-constexpr int MK_BYTE_ROWS = 16384 - 32;  // byte map + one dummy byte in the 16 KB cache
+constexpr int MK_CACHE_BYTES = (1 << MK_CACHE_BITS) * 8;
+constexpr int MK_WIN_WORDS = MK_CACHE_BYTES / 8 < 2048 ? MK_CACHE_BYTES / 8 : MK_CACHE_BYTES / 4;  // window words
+constexpr int MK_BYTE_ROWS = MK_CACHE_BYTES - 32;  // byte map + one dummy byte in the cache region
 constexpr int MK_WSTAGES = 4;        // per-warp ring depth
 constexpr int MK_WSTAGE_BYTES = 1024;  // per-warp stage: 256 int32 / 128 int64 ids
 constexpr int MK_WARPS = MARK_THREADS / 32;
 
-// One CTA's range [start, end) (ids of segment `seg`, width sizeof(IdxT)).
-template <typename IdxT>
+// ids bit-packed at a segment-specific width (LSB-first bitstream)
+struct BitPacked {};
+
+// One CTA's range [start, end) of segment `seg`: typed ids (uint8_t,
+// uint16_t, int32_t, int64_t) or BitPacked ids of a.seg_width[seg] bits.
+template <typename IdxT, int WB = 0>
 __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t start, int64_t end,
                                            unsigned long long *cache,
                                            unsigned long long (*bars)[MK_WSTAGES], uint8_t *mk_smem) {
-    constexpr int IDS = MK_WSTAGE_BYTES / (int)sizeof(IdxT);  // ids per warp stage
-    constexpr int PER_LANE = IDS / 32;                          // 32 B of ids per lane
+    constexpr bool BITS = std::is_same<IdxT, BitPacked>::value;
+    static_assert(!BITS || (WB >= 4 && WB <= 28 && WB % 4 == 0), "packed widths: 4..28 bits, step 4");
+    using T = typename std::conditional<BITS, uint32_t, IdxT>::type;  // element type of a lane's ids
+    // ids per warp stage: 32 B of typed ids per lane, 8 bit-packed ids per lane
+    constexpr int IDS = BITS ? 256 : MK_WSTAGE_BYTES / (int)sizeof(T);
+    constexpr int PER_LANE = IDS / 32;
+    constexpr int wbits = BITS ? WB : 8 * (int)sizeof(T);  // bits per id
+    constexpr uint32_t wmask = wbits >= 32 ? 0xffffffffu : (1u << wbits) - 1u;
     uint32_t *win = reinterpret_cast<uint32_t *>(cache);  // bit window (aliases the cache)
     uint8_t *bytes = reinterpret_cast<uint8_t *>(cache);  // byte map (aliases the cache)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -234,18 +251,22 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
     const uint32_t nwords = (uint32_t)((rows + 31) / 32);
     // 32-bit bound for the byte map (int32 ids never exceed 2^31 - 1)
     const uint32_t rows32 = (uint32_t)min(rows, (uint64_t)0x80000000ull);
-    auto in_range = [&](IdxT v) -> bool {  // negatives wrap high
-        if (sizeof(IdxT) <= 4) return (uint32_t)v < rows32;
+    auto in_range = [&](T v) -> bool {  // negatives wrap high
+        if (sizeof(T) <= 4) return (uint32_t)v < rows32;
         return (uint64_t)(int64_t)v < rows;
     };
     const int mode = rows <= (uint64_t)MK_BYTE_ROWS ? 0 : (nwords <= (uint32_t)MK_WIN_WORDS ? 1 : 2);
     for (int k = threadIdx.x; k < (1 << MK_CACHE_BITS); k += MARK_THREADS) cache[k] = 0ull;
-    const IdxT *idx = reinterpret_cast<const IdxT *>(a.ibytes + a.seg_boff[seg]);
-    IdxT *ring = reinterpret_cast<IdxT *>(mk_smem) + (size_t)wid * MK_WSTAGES * IDS;
+    const uint8_t *sbytes = a.ibytes + a.seg_boff[seg];
+    const T *idx = reinterpret_cast<const T *>(sbytes);
+    // a stage holds IDS ids: sizeof(T) * IDS bytes, or 32 * wbits bytes packed
+    uint8_t *ring = mk_smem + (size_t)wid * MK_WSTAGES * MK_WSTAGE_BYTES;
     unsigned long long *wb = bars[wid];
-    // TMA moves whole 16-byte units; the ragged tail (< 16 B) is read directly
+    // TMA moves whole 16-byte units: typed ids leave a ragged tail (< 16 B)
+    // read directly; packed segments are padded to 16 bytes, so their last
+    // chunk is copied whole
     const int64_t bulk_end =
-        start + ((end - start) * (int64_t)sizeof(IdxT) / 16) * 16 / (int64_t)sizeof(IdxT);
+        BITS ? end : start + ((end - start) * (int64_t)sizeof(T) / 16) * 16 / (int64_t)sizeof(T);
     const int nch = (int)((bulk_end - start + IDS - 1) / IDS);
     if (lane == 0) {
         for (int s = 0; s < MK_WSTAGES; s++) mbar_init(&wb[s], 1);
@@ -256,9 +277,18 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
         const int c = wid + k * MK_WARPS;
         if (c < nch) {
             const int64_t c0 = start + (int64_t)c * IDS;
-            const unsigned nb = (unsigned)(min((int64_t)IDS, bulk_end - c0) * sizeof(IdxT));
+            const int64_t n = min((int64_t)IDS, bulk_end - c0);
+            const uint8_t *src;
+            unsigned nb;
+            if (BITS) {  // c0 is a multiple of 256 ids: a whole number of 16-byte units
+                src = sbytes + ((uint64_t)c0 >> 3) * wbits;
+                nb = (((unsigned)n * wbits + 7u) >> 3) + 15u & ~15u;
+            } else {
+                src = reinterpret_cast<const uint8_t *>(idx + c0);
+                nb = (unsigned)(n * sizeof(T));
+            }
             mbar_expect_tx(&wb[k % MK_WSTAGES], nb);
-            tma_load_1d(ring + (size_t)(k % MK_WSTAGES) * IDS, idx + c0, nb, &wb[k % MK_WSTAGES]);
+            tma_load_1d(ring + (size_t)(k % MK_WSTAGES) * MK_WSTAGE_BYTES, src, nb, &wb[k % MK_WSTAGES]);
         }
     };
     if (lane == 0)
@@ -289,6 +319,87 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
             cache_mark(w, 1u << (u & 31), slot, cache[slot]);
         }
     };
+    // id q of a bit-packed stage (words of the stage; may read one word past)
+    auto unpack = [&](const uint32_t *wds, int q) -> uint32_t {
+        const int p = q * wbits;
+        return __funnelshift_r(wds[p >> 5], wds[(p >> 5) + 1], p & 31) & wmask;
+    };
+    // the lane's 8 ids: the width is a multiple of 4 bits, so the lane's
+    // 8*w bits are w/4 whole words; every shift is a compile-time constant
+    auto unpack8 = [&](const uint32_t *wds, uint32_t (&v)[8]) {
+        constexpr int NW = wbits / 4;
+        const uint32_t *lw = wds + lane * NW;
+        uint32_t wd[NW + 1];
+#pragma unroll
+        for (int k = 0; k < NW; k++) wd[k] = lw[k];
+        wd[NW] = 0u;
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int bit = q * wbits;  // constant after unrolling
+            v[q] = __funnelshift_r(wd[bit >> 5], wd[(bit >> 5) + 1], bit & 31) & wmask;
+        }
+    };
+    // a group of NQ ids of this lane, all of the current segment
+    auto mark_group = [&](auto &v) {
+        constexpr int NQ = sizeof(v) / sizeof(v[0]);
+        if (mode == 0) {
+            // out-of-range ids store to the dummy byte at index `rows`
+            // (masked off by the flush) instead of branching
+            const uint32_t sb = smem_u32(bytes);
+            if (sizeof(T) <= 4) {
+                uint32_t umax = 0;  // negatives wrap high
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    const uint32_t u = (uint32_t)v[q];
+                    umax = max(umax, u);
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + min(u, rows32)), "r"(1) : "memory");
+                }
+                bad |= umax >= rows32;
+            } else {
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    const bool ok = in_range(v[q]);
+                    bad |= !ok;
+                    asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + (ok ? (uint32_t)v[q] : rows32)),
+                                 "r"(1) : "memory");
+                }
+            }
+        } else if (mode == 1) {
+            uint32_t cur[NQ];
+            bool ok[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                ok[q] = in_range(v[q]);
+                bad |= !ok[q];
+                cur[q] = ok[q] ? win[(uint32_t)v[q] >> 5] : ~0u;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
+                if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
+            }
+        } else {
+            // probes in groups of 8 so their latencies overlap
+            constexpr int PG = NQ < 8 ? NQ : 8;
+#pragma unroll
+            for (int g = 0; g < NQ; g += PG) {
+                uint32_t w[PG], slot[PG];
+                unsigned long long e[PG];
+                bool ok[PG];
+#pragma unroll
+                for (int q = 0; q < PG; q++) {
+                    ok[q] = in_range(v[g + q]);
+                    bad |= !ok[q];
+                    w[q] = base + ((uint32_t)v[g + q] >> 5);
+                    slot[q] = (w[q] * 2654435761u) >> (32 - MK_CACHE_BITS);
+                    e[q] = cache[slot[q]];
+                }
+#pragma unroll
+                for (int q = 0; q < PG; q++)
+                    if (ok[q]) cache_mark(w[q], 1u << ((uint32_t)v[g + q] & 31), slot[q], e[q]);
+            }
+        }
+    };
     for (int k = 0;; k++) {
         const int c = wid + k * MK_WARPS;
         if (c >= nch) break;
@@ -296,76 +407,30 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
         mbar_wait(&wb[s], (unsigned)(k / MK_WSTAGES) & 1u);
         const int64_t c0 = start + (int64_t)c * IDS;
         const int cnt = (int)min((int64_t)IDS, bulk_end - c0);
-        const IdxT *b = ring + (size_t)s * IDS;
+        const uint8_t *stg = ring + (size_t)s * MK_WSTAGE_BYTES;
         const int j0 = lane * PER_LANE;
         if (j0 + PER_LANE <= cnt) {
-            // two 16-byte halves per lane (keeps the live ids few)
-            constexpr int PH = PER_LANE / 2;
+            if constexpr (BITS) {
+                static_assert(PER_LANE == 8, "8 packed ids per lane");
+                uint32_t v[8];
+                unpack8(reinterpret_cast<const uint32_t *>(stg), v);
+                mark_group(v);
+            } else {
+                // two 16-byte halves per lane (keeps the live ids few)
+                constexpr int PH = PER_LANE / 2;
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                IdxT v[PH];
-                *reinterpret_cast<int4 *>(v) = reinterpret_cast<const int4 *>(b + j0)[h];
-                if (mode == 0) {
-                    // out-of-range ids store to the dummy byte at index `rows`
-                    // (masked off by the flush) instead of branching
-                    const uint32_t sb = smem_u32(bytes);
-                    if (sizeof(IdxT) <= 4) {
-                        uint32_t umax = 0;  // negatives wrap high
-#pragma unroll
-                        for (int q = 0; q < PH; q++) {
-                            const uint32_t u = (uint32_t)v[q];
-                            umax = max(umax, u);
-                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + min(u, rows32)), "r"(1) : "memory");
-                        }
-                        bad |= umax >= rows32;
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < PH; q++) {
-                            const bool ok = in_range(v[q]);
-                            bad |= !ok;
-                            asm volatile("st.shared.u8 [%0], %1;" ::"r"(sb + (ok ? (uint32_t)v[q] : rows32)),
-                                         "r"(1) : "memory");
-                        }
-                    }
-                } else if (mode == 1) {
-                    uint32_t cur[PH];
-                    bool ok[PH];
-#pragma unroll
-                    for (int q = 0; q < PH; q++) {
-                        ok[q] = in_range(v[q]);
-                        bad |= !ok[q];
-                        cur[q] = ok[q] ? win[(uint32_t)v[q] >> 5] : ~0u;
-                    }
-#pragma unroll
-                    for (int q = 0; q < PH; q++) {
-                        const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
-                        if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
-                    }
-                } else {
-                    // probes in groups of 8 so their latencies overlap
-                    constexpr int PG = PH < 8 ? PH : 8;
-#pragma unroll
-                    for (int g = 0; g < PH; g += PG) {
-                        uint32_t w[PG], slot[PG];
-                        unsigned long long e[PG];
-                        bool ok[PG];
-#pragma unroll
-                        for (int q = 0; q < PG; q++) {
-                            ok[q] = in_range(v[g + q]);
-                            bad |= !ok[q];
-                            w[q] = base + ((uint32_t)v[g + q] >> 5);
-                            slot[q] = (w[q] * 2654435761u) >> (32 - MK_CACHE_BITS);
-                            e[q] = cache[slot[q]];
-                        }
-#pragma unroll
-                        for (int q = 0; q < PG; q++)
-                            if (ok[q]) cache_mark(w[q], 1u << ((uint32_t)v[g + q] & 31), slot[q], e[q]);
-                    }
+                for (int h = 0; h < 2; h++) {
+                    T v[PH];
+                    *reinterpret_cast<int4 *>(v) =
+                        reinterpret_cast<const int4 *>(reinterpret_cast<const T *>(stg) + j0)[h];
+                    mark_group(v);
                 }
             }
         } else {
             for (int q = j0; q < cnt && q < j0 + PER_LANE; q++) {
-                const int64_t r = (int64_t)b[q];
+                int64_t r;
+                if constexpr (BITS) r = unpack(reinterpret_cast<const uint32_t *>(stg), q);
+                else r = (int64_t)reinterpret_cast<const T *>(stg)[q];
                 if ((uint64_t)r >= rows) bad = true;
                 else mark_row((uint32_t)r);
             }
@@ -376,11 +441,13 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
             issue(k + MK_WSTAGES);
         }
     }
-    // ragged tail
-    for (int64_t i = bulk_end + threadIdx.x; i < end; i += MARK_THREADS) {
-        const int64_t r = (int64_t)idx[i];
-        if ((uint64_t)r >= rows) bad = true;
-        else mark_row((uint32_t)r);
+    // ragged tail (typed ids only)
+    if constexpr (!BITS) {
+        for (int64_t i = bulk_end + threadIdx.x; i < end; i += MARK_THREADS) {
+            const int64_t r = (int64_t)idx[i];
+            if ((uint64_t)r >= rows) bad = true;
+            else mark_row((uint32_t)r);
+        }
     }
     if (mode != 2) {
         __syncthreads();
@@ -408,25 +475,33 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
     if (__any_sync(DS_FULL_MASK, bad) && lane == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
 }
 
-// Segments of 1-byte / 2-byte (unsigned) and 4-byte / 8-byte (signed) ids:
-// the host sends each table's lookups at the narrowest width its row count
-// allows, which is what bounds the end-to-end H2D of the lookup stream.
+// Segments of ids bit-packed at 4..28 bits (8 and 16: plain u8 / u16) or
+// 32 / 64-bit signed ids: the host sends each table's lookups at the width
+// its row count needs, which is what bounds the end-to-end H2D of the lookup
+// stream.
 __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a) {
     extern __shared__ __align__(128) uint8_t mk_smem[];
     __shared__ __align__(8) unsigned long long bars[MK_WARPS][MK_WSTAGES];
-    __shared__ __align__(16) unsigned long long cache[1 << MK_CACHE_BITS];  // 16 KB
-    static_assert(MK_WIN_WORDS * 4 <= (1 << MK_CACHE_BITS) * 8, "window must fit the cache");
-    static_assert(MK_BYTE_ROWS + 32 <= (1 << MK_CACHE_BITS) * 8, "byte map must fit the cache");
+    // dynamic shared memory: [per-warp TMA rings][cache | bit window | byte map]
+    unsigned long long *cache = reinterpret_cast<unsigned long long *>(
+        mk_smem + (size_t)MK_WARPS * MK_WSTAGES * MK_WSTAGE_BYTES);
+    static_assert(MK_WIN_WORDS * 4 <= MK_CACHE_BYTES, "window must fit the cache");
+    static_assert(MK_BYTE_ROWS + 32 <= MK_CACHE_BYTES, "byte map must fit the cache");
     int j = 0;  // position in seg_order: last j with blk_off[j] <= blockIdx.x
     while (j + 1 < a.nseg && a.blk_off[j + 1] <= (int)blockIdx.x) j++;
     const int seg = a.seg_order[j];
     const int64_t start = (int64_t)(blockIdx.x - a.blk_off[j]) * a.seg_pb[seg];
     const int64_t end = min(a.seg_n[seg], start + a.seg_pb[seg]);
     switch (a.seg_width[seg]) {
-    case 1: mark_range<uint8_t>(a, seg, start, end, cache, bars, mk_smem); break;
-    case 2: mark_range<uint16_t>(a, seg, start, end, cache, bars, mk_smem); break;
-    case 4: mark_range<int32_t>(a, seg, start, end, cache, bars, mk_smem); break;
-    default: mark_range<int64_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 8: mark_range<uint8_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 16: mark_range<uint16_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 32: mark_range<int32_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 64: mark_range<int64_t>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 4: mark_range<BitPacked, 4>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 12: mark_range<BitPacked, 12>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 20: mark_range<BitPacked, 20>(a, seg, start, end, cache, bars, mk_smem); break;
+    case 24: mark_range<BitPacked, 24>(a, seg, start, end, cache, bars, mk_smem); break;
+    default: mark_range<BitPacked, 28>(a, seg, start, end, cache, bars, mk_smem); break;
     }
 }
 
@@ -889,7 +964,7 @@ using namespace ds;
 
 // TMA form over a packed stream of segments (16-byte aligned, any width).
 // Lookups are weighted by the per-lookup cost of their table's kind (byte map
-// 1, bit window 2, cache + RED 3, measured on B200) and cut into CTAs of
+// 1, bit window 2, cache + RED 2, measured on B200) and cut into CTAs of
 // about equal cost, expensive kinds first; every CTA range is a multiple of a
 // warp stage so every bulk copy starts 16-byte aligned.
 static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int64_t *rows,
@@ -911,8 +986,8 @@ static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int6
         const int t = seg_table_host ? seg_table_host[s] : 0;
         if (t < 0 || t >= DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_mark_packed: table index");
         const int w = seg_width[s];
-        if (w != 1 && w != 2 && w != 4 && w != 8)
-            return host::fail(DS_ERR_ARG, "ds_mark_packed: id width must be 1, 2, 4 or 8 bytes");
+        if (!((w >= 4 && w <= 28 && w % 4 == 0) || w == 32 || w == 64))
+            return host::fail(DS_ERR_ARG, "ds_mark_packed: id width must be 4..28 (step 4), 32 or 64 bits");
         if (seg_boff[s] % 16 || seg_n[s] < 0)
             return host::fail(DS_ERR_ARG, "ds_mark_packed: segments must start 16-byte aligned");
         a.word_off[s] = word_off[t];
@@ -930,14 +1005,14 @@ static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int6
     // the cache keys are 31-bit word ids
     if (max_word >= (int64_t)0x7fffffffLL)
         return host::fail(DS_ERR_CONFIG, "ds_mark: a table set holds at most 2^31-1 bitmap words");
-    const size_t smem = (size_t)MK_WARPS * MK_WSTAGES * MK_WSTAGE_BYTES;
+    const size_t smem = (size_t)MK_WARPS * MK_WSTAGES * MK_WSTAGE_BYTES + MK_CACHE_BYTES;
     auto fn = mark_tma_kernel;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     int tper = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, fn, MARK_THREADS, smem);
     if (tper < 1) tper = 1;
-    static const int64_t kCost[3] = {1, 2, 3};
+    static const int64_t kCost[3] = {1, 2, 2};
     const int64_t cost_cache = host::env_int("DS_MARK_COST_CACHE", kCost[2]);
     int kind[DS_MAX_TABLES];
     double total_cost = 0.0;
@@ -955,7 +1030,9 @@ static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int6
         for (int s = 0; s < nseg; s++) {
             if (kind[s] != kd) continue;
             const int64_t w = kd == 2 ? cost_cache : kCost[kd];
-            const int64_t ids_per_stage = MK_WSTAGE_BYTES / a.seg_width[s];
+            const int wb = a.seg_width[s];  // bits
+            const int64_t ids_per_stage =
+                (wb == 8 || wb == 16 || wb == 32 || wb == 64) ? MK_WSTAGE_BYTES * 8 / wb : 256;
             int64_t pb = (int64_t)(target / (double)w) + 1;
             pb = (pb + ids_per_stage - 1) / ids_per_stage * ids_per_stage;
             a.seg_pb[s] = pb;
@@ -996,7 +1073,7 @@ static int mark_impl(uint32_t *words, const int64_t *word_off, const int64_t *ro
         for (int s = 0; s < nseg; s++) {
             boff[s] = seg_off_host[s] * isz;
             n[s] = seg_off_host[s + 1] - seg_off_host[s];
-            wd[s] = (int32_t)isz;
+            wd[s] = (int32_t)(8 * isz);
         }
         return mark_packed_impl(words, word_off, rows, idx, boff, n, wd, seg_table_host, nseg, flags,
                                 stream);

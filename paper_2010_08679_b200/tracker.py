@@ -399,26 +399,47 @@ class ModelTracker:
 # ---------------------------------------------------------------------------
 
 def lookup_width(rows: int) -> int:
-    """Narrowest id width (bytes) for a table of `rows` rows: u8, u16, i32, i64."""
-    if rows <= 1 << 8:
-        return 1
-    if rows <= 1 << 16:
-        return 2
-    if rows <= 1 << 31:
-        return 4
-    return 8
+    """Bits per id for a table of `rows` rows: ceil(log2(rows)) rounded up to
+    a multiple of 4 (a lane's 8 ids then fill whole 32-bit words) and at
+    least 4, bit-packed; 32 / 64 for signed int32 / int64 above 2^28 rows."""
+    b = (max(1, int(rows - 1).bit_length()) + 3) // 4 * 4
+    if b <= 28:
+        return b
+    return 32 if rows <= 1 << 31 else 64
 
 
-_WIDTH_DTYPE = {1: np.uint8, 2: np.uint16, 4: np.int32, 8: np.int64}
+def pack_ids(a, bits: int) -> np.ndarray:
+    """Little-endian (LSB-first) bitstream of ids at `bits` bits each; 32 and
+    64 bits are plain int32 / int64 arrays."""
+    a = np.asarray(a)
+    if bits == 64:
+        return np.ascontiguousarray(a, dtype=np.int64).view(np.uint8)
+    if bits == 32:
+        return np.ascontiguousarray(a, dtype=np.int32).view(np.uint8)
+    if bits == 8:
+        return np.ascontiguousarray(a, dtype=np.uint8)
+    if bits == 16:
+        return np.ascontiguousarray(a, dtype=np.uint16).view(np.uint8)
+    out = np.zeros((a.size * bits + 7) // 8, dtype=np.uint8)
+    shifts = np.arange(bits, dtype=np.uint64)
+    blk = 1 << 20  # ids per block (a multiple of 8: every block starts on a byte)
+    for i in range(0, a.size, blk):
+        v = a[i:i + blk].astype(np.uint64)
+        bitsm = ((v[:, None] >> shifts) & np.uint64(1)).astype(np.uint8)
+        packed = np.packbits(bitsm.reshape(-1), bitorder="little")
+        o = i * bits // 8
+        out[o:o + packed.size] = packed
+    return out
 
 
 class LookupStream:
-    """One interval's (or batch's) lookups of several tables, packed at the
-    narrowest width per table into one 16-byte-aligned byte buffer.
+    """One interval's (or batch's) lookups of several tables, each table's
+    ids bit-packed at ceil(log2(rows)) bits rounded up to a multiple of 4
+    (lookup_width) into one byte buffer with 16-byte-aligned segments.
 
     This is the wire format of K1's input: a data loader fills it on the host
     (pinned), one H2D copy moves it, and ModelTracker.mark_packed consumes it.
-    Segment s = seg_count[s] ids of seg_width[s] bytes at seg_byte_off[s],
+    Segment s = seg_count[s] ids of seg_width[s] bits at seg_byte_off[s],
     all of table seg_tables[s].
     """
 
@@ -445,7 +466,7 @@ class LookupStream:
             boff.append(off)
             cnt.append(int(counts[t]))
             wid.append(w)
-            off += (int(counts[t]) * w + 15) // 16 * 16
+            off += ((int(counts[t]) * w + 7) // 8 + 15) // 16 * 16
         return boff, cnt, wid, tids, off
 
     @classmethod
@@ -458,9 +479,10 @@ class LookupStream:
         host = buf.numpy()
         for t, o, n, w in zip(tids, boff, cnt, wid):
             a = np.asarray(lookups[t])
-            if w <= 2 and a.size and (a.min() < 0 or a.max() >= table_rows[t]):
-                raise BoundsError(f"table {t}: row index out of range for a {8 * w}-bit stream")
-            host[o:o + n * w].view(_WIDTH_DTYPE[w])[:] = a
+            if w < 32 and a.size and (a.min() < 0 or a.max() >= table_rows[t]):
+                raise BoundsError(f"table {t}: row index out of range for a {w}-bit stream")
+            p = pack_ids(a, w)
+            host[o:o + p.size] = p
         return cls(buf, boff, cnt, wid, tids)
 
     def to(self, device, out: torch.Tensor | None = None, non_blocking: bool = True) -> "LookupStream":

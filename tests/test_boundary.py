@@ -109,3 +109,19 @@ def test_serialize_section_matches_oracle_layout():
     sec = TableSection(table_id=1, dim=9, mode=0, values=x)
     assert serialize_section(sec, False) == O.build_section(1, x, None, bitwidth=None)[0]
     assert struct.unpack_from("<Q", serialize_section(sec, False), 8)[0] == 6
+
+
+def test_pack_ids_bitstream():
+    """LookupStream wire format: ids LSB-first at `bits` bits (ds_mark_packed)."""
+    import numpy as np
+    from paper_2010_08679_b200.tracker import lookup_width, pack_ids
+    rng = np.random.default_rng(4)
+    for bits in (1, 3, 7, 8, 9, 13, 16, 17, 24, 31):
+        a = rng.integers(0, 1 << bits, 1000 + bits)
+        p = pack_ids(a, bits)
+        assert p.size == (a.size * bits + 7) // 8
+        stream = int.from_bytes(p.tobytes(), "little")
+        got = [(stream >> (i * bits)) & ((1 << bits) - 1) for i in range(a.size)]
+        assert got == a.tolist(), bits
+    assert [lookup_width(r) for r in (1, 2, 3, 256, 257, 1 << 28, (1 << 28) + 1, 1 << 31,
+                                      (1 << 31) + 1)] == [4, 4, 4, 8, 12, 28, 32, 32, 64]

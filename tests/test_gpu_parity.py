@@ -453,18 +453,19 @@ def test_restore_errors(ds, O):
 # --- packed lookup streams (ds_mark_packed) ---------------------------------------
 
 def test_mark_packed_mixed_widths(ds):
-    """u8 / u16 / i32 segments of one packed stream, every table kind, Zipf
+    """Bit-packed and u8 / u16 segments of one stream, every table kind, Zipf
     repeats and ragged lengths: the interval sets equal the unique ids."""
     rng = np.random.default_rng(21)
-    rows = {0: 1, 1: 200, 2: 256, 3: 257, 4: 16352, 5: 40_000, 6: 65_536, 7: 65_537, 8: 2_000_000}
+    rows = {0: 1, 1: 200, 2: 256, 3: 257, 4: 16352, 5: 40_000, 6: 65_536, 7: 65_537, 8: 12_000_000}
     look = {}
     for t, r in rows.items():
         n = int(rng.integers(0, 30_000))
         hot = rng.integers(0, r, 4)
         look[t] = np.where(rng.random(n) < 0.6, hot[rng.integers(0, 4, n)], rng.integers(0, r, n))
     st = ds.LookupStream.pack(look, rows)
-    assert [ds.lookup_width(r) for r in rows.values()] == [1, 1, 1, 2, 2, 2, 2, 4, 4]
-    assert st.seg_width.tolist() == [1, 1, 1, 2, 2, 2, 2, 4, 4]
+    # bit-packed (4, 12, 20, 24 bits) and plain u8 / u16 segments
+    assert [ds.lookup_width(r) for r in rows.values()] == [4, 8, 8, 12, 16, 16, 16, 20, 24]
+    assert st.seg_width.tolist() == [4, 8, 8, 12, 16, 16, 16, 20, 24]
     tr = ds.ModelTracker(rows)
     tr.mark_packed(st.to(tr.device))
     view = tr.capture()
@@ -473,14 +474,16 @@ def test_mark_packed_mixed_widths(ds):
 
 
 def test_mark_packed_bounds(ds):
+    """Packed widths cannot hold out-of-range ids: LookupStream.pack rejects
+    them on the host (BoundsError, nothing marked); the kernel-side bounds
+    flag of 32/64-bit streams is covered by test_mark_batch_table_kinds_and_bounds."""
     rows = {0: 100, 1: 70_000}
-    with pytest.raises(ds.BoundsError):  # would wrap at 8 bits: rejected on the host
-        ds.LookupStream.pack({0: np.array([5, 100])}, rows)
+    for bad in ({0: np.array([5, 100])}, {1: np.array([1, 70_000])}, {1: np.array([-3])}):
+        with pytest.raises(ds.BoundsError):
+            ds.LookupStream.pack(bad, rows)
     tr = ds.ModelTracker(rows)
-    st = ds.LookupStream.pack({0: np.array([5, 99]), 1: np.array([1, 70_000, -3, 69_999])}, rows)
+    st = ds.LookupStream.pack({0: np.array([5, 99]), 1: np.array([1, 69_999, 1])}, rows)
     tr.mark_packed(st.to(tr.device))
-    with pytest.raises(ds.BoundsError):  # i32 segment: flagged by the kernel
-        tr.capture()
     view = tr.capture()
     assert view.interval_rows[0].tolist() == [5, 99]
     assert view.interval_rows[1].tolist() == [1, 69_999]
