@@ -336,6 +336,8 @@ def run_ours(args):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
+        # NCCL's banner/debug output goes to stderr: stdout carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     from paper_2010_08679_b200 import _lib as dslib
     if args.l2_fetch:
@@ -373,14 +375,23 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up: W steps, then keep stepping until the clocks have ramped (>= 0.3 s)
+    # warm-up: W steps, then keep stepping until the clocks have ramped
+    # (>= 0.3 s).  Every step holds a collective at N > 1, so all ranks run
+    # the same number of ramp steps (the max of their own estimates).
     for _ in range(max(3, args.warmup)):
         ck.step(stream)
     torch.cuda.synchronize()
-    t_end = time.perf_counter() + 0.3
-    while time.perf_counter() < t_end:
+    t0 = time.perf_counter()
+    ck.step(stream)
+    torch.cuda.synchronize()
+    n_ramp = int(0.3 / max(time.perf_counter() - t0, 1e-6)) + 1
+    if world > 1:
+        nt_ = torch.tensor([n_ramp], dtype=torch.int64, device=dev)
+        dist.all_reduce(nt_, op=dist.ReduceOp.MAX)
+        n_ramp = int(nt_.item())
+    for _ in range(min(n_ramp, 20000)):
         ck.step(stream)
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
     ck.fetch()  # raises any flagged data error of the warm-up steps
 
     # ---- device-timed region: exactly K steps --------------------------------------
