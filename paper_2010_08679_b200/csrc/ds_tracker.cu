@@ -763,20 +763,16 @@ struct Cap3Args {
     int fold;
 };
 
-// table of chunk c, once per CTA (binary search, broadcast through shared memory)
+// table of chunk c: binary search over the kernel parameters (every thread,
+// no barrier)
 __device__ __forceinline__ int cap3_table(const Cap3Args &a, int c) {
-    __shared__ int s_t;
-    if (threadIdx.x == 0) {
-        int lo = 0, hi = a.ntables - 1;  // last t with chunk_off[t] <= c
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (a.chunk_off[mid] <= c) lo = mid;
-            else hi = mid - 1;
-        }
-        s_t = lo;
+    int lo = 0, hi = a.ntables - 1;  // last t with chunk_off[t] <= c
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.chunk_off[mid] <= c) lo = mid;
+        else hi = mid - 1;
     }
-    __syncthreads();
-    return s_t;
+    return lo;
 }
 
 // the thread's C3_WPT words of chunk c: one 16-byte load when the table's
@@ -818,17 +814,6 @@ __device__ __forceinline__ unsigned long long cap3_block_sum(unsigned long long 
     return s;
 }
 
-// packed ids before chunk x: the sums of the whole 256-chunk groups before it
-// plus the chunks of its own group before it (one load per thread)
-__device__ __forceinline__ unsigned long long cap3_base(const Cap3Args &a, int x,
-                                                        unsigned long long *s_red) {
-    unsigned long long v = 0;
-    const int g = x >> 8, g0 = g << 8;
-    for (int i = threadIdx.x; i < g; i += CF_THREADS) v += __ldcg(a.super + i);
-    if (g0 + (int)threadIdx.x < x) v += __ldcg(a.cnt + g0 + threadIdx.x);
-    return cap3_block_sum(v, s_red);
-}
-
 // pass 1: per-chunk popcounts, and their 256-chunk group sums
 __global__ void __launch_bounds__(CF_THREADS) cap3_count_kernel(const Cap3Args a) {
     __shared__ unsigned long long s_red[CF_THREADS / 32];
@@ -852,50 +837,80 @@ static_assert(CAP3_STAGE * 4 <= 48 * 1024, "stage must fit static shared memory"
 
 // pass 2: the chunk's base from the group sums, its sorted ids (staged in
 // shared memory, coalesced int64 stores), the per-table counts (by each
-// table's last chunk), then the fold
+// table's last chunk), then the fold.  Two CTA barriers: one reduction that
+// yields the thread's scan offset, the chunk's base and (last chunks) the
+// table's start together, and one before the staged ids leave.
 __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a) {
-    __shared__ unsigned long long s_red[CF_THREADS / 32];
-    __shared__ unsigned long long s_warp[CF_THREADS / 32];
+    constexpr int NWP = CF_THREADS / 32;
+    __shared__ unsigned long long s_cnt[NWP], s_base[NWP], s_start[NWP];
     __shared__ uint32_t s_ids[CAP3_STAGE];
-    __shared__ bool s_last;
     const int c = blockIdx.x, t = cap3_table(a, c);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool last = c == a.chunk_off[t + 1] - 1;  // this table's last chunk
     uint32_t iv[C3_WPT], uv[C3_WPT];
     int64_t w0, wend;
     cap3_load(a, c, t, iv, uv, w0, wend);
-    const unsigned long long b = cap3_base(a, c, s_red);
     unsigned ci = 0, cu = 0;
 #pragma unroll
     for (int k = 0; k < C3_WPT; k++) {
         ci += __popc(iv[k]);
         cu += __popc(uv[k]);
     }
-    // block exclusive scan of packed (cu << 32 | ci)
+    // packed (union << 32 | interval) ids before chunk x: the 256-chunk group
+    // sums before it plus its own group's chunks before it (one load each)
+    auto part = [&](int x) -> unsigned long long {
+        unsigned long long v = 0;
+        const int g = x >> 8, g0 = g << 8;
+        for (int i = threadIdx.x; i < g; i += CF_THREADS) v += __ldcg(a.super + i);
+        if (g0 + (int)threadIdx.x < x) v += __ldcg(a.cnt + g0 + threadIdx.x);
+        return v;
+    };
     const unsigned long long p = (unsigned long long)ci | ((unsigned long long)cu << 32);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long x = p;
+    unsigned long long x = p, pb = part(c), ps = last ? part((int)a.chunk_off[t]) : 0ull;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(DS_FULL_MASK, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    unsigned long long wbase = 0, tot = 0;
 #pragma unroll
-    for (int k = 0; k < CF_THREADS / 32; k++) {
-        const unsigned long long sw = s_warp[k];
+    for (int o = 16; o > 0; o >>= 1) {
+        pb += __shfl_xor_sync(DS_FULL_MASK, pb, o);
+        ps += __shfl_xor_sync(DS_FULL_MASK, ps, o);
+    }
+    if (lane == 31) s_cnt[wid] = x;
+    if (lane == 0) {
+        s_base[wid] = pb;
+        s_start[wid] = ps;
+    }
+    __syncthreads();  // (1): every read of super/cnt of this CTA is done
+    if (threadIdx.x == 0) {
+        // the last CTA past this point clears the group sums for the next call
+        if (atomicAdd(a.ticket, 1u) == gridDim.x - 1) {
+            for (int i = 0; i <= (a.nchunks >> 8); i++) a.super[i] = 0ull;
+            *a.ticket = 0u;
+        }
+    }
+    unsigned long long wbase = 0, tot = 0, b = 0, start = 0;
+#pragma unroll
+    for (int k = 0; k < NWP; k++) {
+        const unsigned long long sw = s_cnt[k];
         wbase += k < wid ? sw : 0ull;
         tot += sw;
+        b += s_base[k];
+        start += s_start[k];
     }
     const unsigned long long excl = wbase + x - p;
     const int64_t crow0 = (w0 - threadIdx.x * C3_WPT - a.word_off[t]) * 32;  // chunk's first row
     const unsigned lrow0 = threadIdx.x * C3_WPT * 32;                         // thread's first row
+    // one scope is emitted per call (capture_into); both share the stage in
+    // two rounds when both are asked for
     for (int scope = 0; scope < 2; scope++) {
         int64_t *out = scope ? a.ids_uni : a.ids_int;
         if (!out) continue;
         const unsigned n = (unsigned)(scope ? tot >> 32 : tot & 0xffffffffu);
         unsigned o = (unsigned)(scope ? excl >> 32 : excl & 0xffffffffu);
         const int64_t gbase = scope ? (int64_t)(b >> 32) : (int64_t)(uint32_t)b;
+        if (scope == 1 && a.ids_int) __syncthreads();  // the interval round left the stage
 #pragma unroll
         for (int k = 0; k < C3_WPT; k++) {
             uint32_t m = scope ? uv[k] : iv[k];
@@ -904,23 +919,19 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
                 m &= m - 1;
             }
         }
-        __syncthreads();
+        __syncthreads();  // (2)
         for (unsigned j = threadIdx.x; j < n; j += CF_THREADS)
             __stcs(out + gbase + j, crow0 + s_ids[j]);
-        __syncthreads();
     }
     // per-table counts: written by the table's last chunk
-    if (c == a.chunk_off[t + 1] - 1) {
-        const unsigned long long start = cap3_base(a, (int)a.chunk_off[t], s_red);
+    if (last && threadIdx.x == 0) {
         const unsigned long long end = b + tot;
         const int nt = a.ntables;
-        if (threadIdx.x == 0) {
-            a.counts[t] = (int64_t)((uint32_t)end - (uint32_t)start);
-            a.counts[nt + 1 + t] = (int64_t)((end >> 32) - (start >> 32));
-            if (t == nt - 1) {
-                a.counts[nt] = (int64_t)(uint32_t)end;
-                a.counts[2 * nt + 1] = (int64_t)(end >> 32);
-            }
+        a.counts[t] = (int64_t)((uint32_t)end - (uint32_t)start);
+        a.counts[nt + 1 + t] = (int64_t)((end >> 32) - (start >> 32));
+        if (t == nt - 1) {
+            a.counts[nt] = (int64_t)(uint32_t)end;
+            a.counts[2 * nt + 1] = (int64_t)(end >> 32);
         }
     }
     if (a.fold) {  // reset_interval (1) / reset_baseline (2)
@@ -944,17 +955,6 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
                 }
             }
         }
-    }
-    // the last CTA clears the group sums for the next call
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        for (int i = threadIdx.x; i <= (a.nchunks >> 8); i += CF_THREADS) a.super[i] = 0ull;
-        if (threadIdx.x == 0) *a.ticket = 0u;
     }
 }
 
