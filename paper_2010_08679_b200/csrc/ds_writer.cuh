@@ -481,6 +481,87 @@ __device__ __forceinline__ int tile_table(const int64_t *s_sched, int nt, int64_
 }
 
 // ---------------------------------------------------------------------------
+// MODE 1 exact fixup, in place: for the rows of a chunk whose codes the hot
+// loop could not certify (a code within the fp32 guard band of a tie, or a
+// range outside fp32's comfort zone; ~0.3% of rows), re-check the ambiguous
+// elements in exact f64 from the row still in registers, rewrite the
+// record's packed codes in the stage if any code changes, and swap the row's
+// error term.  Warp-collective (every lane calls it when any row needs it).
+// ---------------------------------------------------------------------------
+template <int G, int C, int VEC, bool PAD, bool CONTIG>
+__device__ __forceinline__ void fix_rows_inline(const WriterArgs &a, const float (&x)[C * VEC],
+                                                int lig, int d, bool mine, uint8_t *rec,
+                                                uint8_t *cs, WAcc &acc) {
+    using Lay = Layout<G, C, VEC>;
+    constexpr int EPL = C * VEC;
+    auto el = [&](int k) -> int { return CONTIG ? EPL * lig + k : Lay::elem(lig, k); };
+    float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < EPL; k++)
+        if (!PAD || el(k) < d) {
+            mn = fminf(mn, x[k]);
+            mx = fmaxf(mx, x[k]);
+        }
+    const float lo = grp_min<G>(mn), hi = grp_max<G>(mx);
+    const RowQ rq = make_rowq(lo, hi, a.L, a.invL);
+    int qfast[EPL], qex[EPL];
+    bool changed = false;
+#pragma unroll
+    for (int k = 0; k < EPL; k++) {
+        const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
+        const float qm = __fadd_rn(v, 12582912.0f);
+        qfast[k] = __float_as_int(qm) & 0x3fffff;
+        qex[k] = qfast[k];
+        const bool in = mine && (!PAD || el(k) < d);
+        if (in && (rq.mode == 2 || fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))) > 0.5f - rq.eps)) {
+            qex[k] = code_exact_slow(x[k], lo, hi, rq.s, a.L);
+            acc.n_exact_codes++;
+            changed |= qex[k] != qfast[k];
+        }
+    }
+    // a fast code was wrong (exact ties; rare), or the range is outside
+    // fp32's comfort zone (the hot loop left the row's error out)
+    const int any_changed = grp_or<G>(changed ? 1 : 0);  // every lane shuffles
+    const bool row_changed = mine && (rq.mode == 2 || any_changed != 0);
+    if (__any_sync(DS_FULL_MASK, row_changed)) {
+        double sf = 0.0, se = 0.0;
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            const int e = el(k);
+            if (row_changed && e < d) {
+                const double ef = __dsub_rn((double)x[k], (double)deq_exact(qfast[k], lo, rq.s));
+                const double ee = __dsub_rn((double)x[k], (double)deq_exact(qex[k], lo, rq.s));
+                sf = fma(ef, ef, sf);
+                se = fma(ee, ee, se);
+                cs[e] = (uint8_t)qex[k];
+            }
+        }
+        sf = grp_sumd<G>(sf);
+        se = grp_sumd<G>(se);
+        if (row_changed && lig == 0)
+            acc.err += (se > 0.0 ? se * rsqrt(se) : 0.0) -
+                       (rq.mode == 2 || !(sf > 0.0) ? 0.0 : sf * rsqrt(sf));
+        __syncwarp();
+        if (row_changed) {  // rewrite the record's packed codes (LSB-first bitstream)
+            uint8_t *pk = rec + a.code_off;
+            const int N = a.bitwidth;
+            for (int b = lig; b < a.packed; b += G) {
+                const int bit0 = 8 * b;
+                const int j0 = bit0 / N, j1 = min(d - 1, (bit0 + 7) / N);
+                uint32_t v = 0;
+                for (int j = j0; j <= j1; j++) {
+                    const int pos = j * N - bit0;
+                    const uint32_t cv = cs[j];
+                    v |= pos >= 0 ? (cv << pos) : (cv >> (-pos));
+                }
+                pk[b] = (uint8_t)v;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // MODE 1 fixup: re-code, in exact f64, the rows of one warp-tile that the
 // hot loop flagged (a code within the fp32 guard band of a tie, or a range
 // outside fp32's comfort zone; ~0.3% of rows on realistic data).  Called by
@@ -605,6 +686,9 @@ __device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
 #ifndef DS_WRITER_MINB
 #define DS_WRITER_MINB 2
 #endif
+#ifndef DS_FIX_INLINE
+#define DS_FIX_INLINE 1  // 0: flagged rows always re-coded in a pass after the warp's tiles
+#endif
 #ifndef DS_WRITER_NS
 #define DS_WRITER_NS 3
 #endif
@@ -620,6 +704,9 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
     constexpr int EPL = C * VEC;
     constexpr int RPC = 32 / G;  // rows per chunk
     constexpr int NS = writer_stages<G>();
+    // one-lane rows re-code flagged rows in place (measured faster); wider
+    // groups keep the after-loop pass (fewer live registers in the hot loop)
+    constexpr bool FIXIN = DS_FIX_INLINE && G == 1;
     const int TR = a.tile_rows;  // records per tile: 32, fewer for huge records (host)
     const int NCH = TR / RPC;    // chunks per tile (the host keeps NCH >= NS - 1)
     extern __shared__ __align__(16) uint8_t smem[];
@@ -757,7 +844,12 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
                 const bool fix = code_row<G, C, VEC, MODE, PAD, VEC == 4 && G == 1>(a, td, x, row, valid, valid ? loc : 0,
                                                                 stage + r * a.rec, codes + slot * d,
                                                                 exact + slot * (d + 8), lig, d, acc);
-                if (MODE == 1) {  // record r's flag to lane r
+                if (MODE == 1 && FIXIN) {
+                    // exact fixup now, from the registers (no second pass)
+                    if (__any_sync(DS_FULL_MASK, fix))
+                        fix_rows_inline<G, C, VEC, PAD, VEC == 4 && G == 1>(a, x, lig, d, fix, stage + r * a.rec,
+                                                                            codes + slot * d, acc);
+                } else if (MODE == 1) {  // record r's flag to lane r
                     const bool f = __shfl_sync(DS_FULL_MASK, fix, ((lane - sub * RPC) & (RPC - 1)) * G);
                     if (lane >= sub * RPC && lane < (sub + 1) * RPC) row_fix |= f;
                 }
@@ -765,7 +857,7 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
                 cst = cst + 1 == NS ? 0 : cst + 1;
             }
             irel--;  // the next tile becomes the current one
-            if (MODE == 1) {
+            if (MODE == 1 && !FIXIN) {
                 const unsigned fm = __ballot_sync(DS_FULL_MASK, row_fix);
                 if (lane == 0) a.fix_mask[gw + (int64_t)j * nwarps] = fm;
             }
@@ -776,7 +868,7 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
             nxt = far;
         }
         cp_async_wait<0>();  // nothing may land after the warp exits
-        if (MODE == 1) {
+        if (MODE == 1 && !FIXIN) {
             // exact re-coding of this warp's flagged records (its tiles, in order)
             __syncwarp();
             for (int64_t tile = gw; tile < total_tiles; tile += nwarps) {
