@@ -743,17 +743,29 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
         const int nwc = blockDim.x >> 5;  // warps per CTA (fewer for huge records)
         const int64_t gw = (int64_t)blockIdx.x * nwc + wid;
         const int64_t nwarps = (int64_t)gridDim.x * nwc;
+        // multi-lane rows: each warp codes one contiguous run of tiles (ids and
+        // records contiguous); one-lane rows: tiles strided over the warps
+        // (measured faster there).  Either way a warp's tiles only move
+        // forward, so the table search is incremental.
+        constexpr bool RUN = G > 1;
+        const int64_t tpw = (total_tiles + nwarps - 1) / nwarps;
+        const int64_t tbeg = RUN ? min(total_tiles, gw * tpw) : gw;
+        const int64_t tend = RUN ? min(total_tiles, tbeg + tpw) : total_tiles;
+        const int64_t tstep = RUN ? 1 : nwarps;
+        int tcur = tbeg < tend ? tile_table(s_sched, nt, tbeg, lane) : 0;  // table of the newest tinfo
         // tile j of this warp: table, first record, records, and lane's row id
         struct TI {
             int t, nrow;
             int64_t i0, loc;  // loc: table-local row of record `lane` (-1: none / invalid)
             bool ok;
         };
-        auto tinfo = [&](int j) -> TI {
+        auto tinfo = [&](int j) -> TI {  // called for j = 0, 1, 2, ... in order
             TI r;
-            const int64_t tile = gw + (int64_t)j * nwarps;
-            r.ok = tile < total_tiles;
-            r.t = r.ok ? tile_table(s_sched, nt, tile, lane) : 0;
+            const int64_t tile = tbeg + (int64_t)j * tstep;
+            r.ok = tile < tend;
+            if (r.ok)
+                while (tcur + 1 < nt && s_sched[tcur + 1] <= tile) tcur++;  // warp-uniform
+            r.t = r.ok ? tcur : 0;
             r.i0 = r.ok ? (tile - s_sched[r.t]) * TR : 0;
             r.nrow = r.ok ? (int)min((int64_t)TR, s_sched[nt + 1 + r.t] - r.i0) : 0;
             r.loc = -1;
@@ -859,7 +871,7 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
             irel--;  // the next tile becomes the current one
             if (MODE == 1 && !FIXIN) {
                 const unsigned fm = __ballot_sync(DS_FULL_MASK, row_fix);
-                if (lane == 0) a.fix_mask[gw + (int64_t)j * nwarps] = fm;
+                if (lane == 0) a.fix_mask[tbeg + (int64_t)j * tstep] = fm;
             }
             const int64_t dst = s_sec[cur.t] + (a.write_headers ? DS_HEADER_SIZE : 0) + cur.i0 * a.rec;
             copy_out(a.payload + dst, stage, (int64_t)cur.nrow * a.rec, lane, 32);
@@ -871,7 +883,7 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
         if (MODE == 1 && !FIXIN) {
             // exact re-coding of this warp's flagged records (its tiles, in order)
             __syncwarp();
-            for (int64_t tile = gw; tile < total_tiles; tile += nwarps) {
+            for (int64_t tile = tbeg; tile < tend; tile += tstep) {
                 const unsigned m = a.fix_mask[tile];
                 if (!m) continue;
                 const int t = tile_table(s_sched, nt, tile, lane);
