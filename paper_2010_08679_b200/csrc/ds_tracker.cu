@@ -239,7 +239,8 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
     static_assert(!BITS || (WB >= 4 && WB <= 28 && WB % 4 == 0), "packed widths: 4..28 bits, step 4");
     using T = typename std::conditional<BITS, uint32_t, IdxT>::type;  // element type of a lane's ids
     // ids per warp stage: 32 B of typed ids per lane, 8 bit-packed ids per lane
-    constexpr int IDS = BITS ? 256 : MK_WSTAGE_BYTES / (int)sizeof(T);
+    // (packed: 16 ids per lane while a stage of 512 fits the 1 KB ring slot)
+    constexpr int IDS = BITS ? (WB <= 16 ? 512 : 256) : MK_WSTAGE_BYTES / (int)sizeof(T);
     constexpr int PER_LANE = IDS / 32;
     constexpr int wbits = BITS ? WB : 8 * (int)sizeof(T);  // bits per id
     constexpr uint32_t wmask = wbits >= 32 ? 0xffffffffu : (1u << wbits) - 1u;
@@ -326,9 +327,9 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
     };
     // the lane's 8 ids: the width is a multiple of 4 bits, so the lane's
     // 8*w bits are w/4 whole words; every shift is a compile-time constant
-    auto unpack8 = [&](const uint32_t *wds, uint32_t (&v)[8]) {
-        constexpr int NW = wbits / 4;
-        const uint32_t *lw = wds + lane * NW;
+    auto unpack8 = [&](const uint32_t *wds, int grp, uint32_t (&v)[8]) {
+        constexpr int NW = wbits / 4;  // words per 8 ids
+        const uint32_t *lw = wds + (lane * (PER_LANE / 8) + grp) * NW;
         uint32_t wd[NW + 1];
 #pragma unroll
         for (int k = 0; k < NW; k++) wd[k] = lw[k];
@@ -411,10 +412,13 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
         const int j0 = lane * PER_LANE;
         if (j0 + PER_LANE <= cnt) {
             if constexpr (BITS) {
-                static_assert(PER_LANE == 8, "8 packed ids per lane");
-                uint32_t v[8];
-                unpack8(reinterpret_cast<const uint32_t *>(stg), v);
-                mark_group(v);
+                static_assert(PER_LANE % 8 == 0, "groups of 8 packed ids per lane");
+#pragma unroll
+                for (int grp = 0; grp < PER_LANE / 8; grp++) {
+                    uint32_t v[8];
+                    unpack8(reinterpret_cast<const uint32_t *>(stg), grp, v);
+                    mark_group(v);
+                }
             } else {
                 // two 16-byte halves per lane (keeps the live ids few)
                 constexpr int PH = PER_LANE / 2;
@@ -1032,7 +1036,8 @@ static int mark_packed_impl(uint32_t *words, const int64_t *word_off, const int6
             const int64_t w = kd == 2 ? cost_cache : kCost[kd];
             const int wb = a.seg_width[s];  // bits
             const int64_t ids_per_stage =
-                (wb == 8 || wb == 16 || wb == 32 || wb == 64) ? MK_WSTAGE_BYTES * 8 / wb : 256;
+                (wb == 8 || wb == 16 || wb == 32 || wb == 64) ? MK_WSTAGE_BYTES * 8 / wb
+                                                              : (wb <= 16 ? 512 : 256);  // mark_range IDS
             int64_t pb = (int64_t)(target / (double)w) + 1;
             pb = (pb + ids_per_stage - 1) / ids_per_stage * ids_per_stage;
             a.seg_pb[s] = pb;
