@@ -78,7 +78,7 @@ METRIC = "checkpointed GB/s of embedding rows (track+quantize+pack) at 1/2/4/8 B
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--seed", type=int, default=0)
@@ -116,7 +116,7 @@ def workload_desc(w):
 
 
 # --------------------------------------------------------------------------------
-# clocks (NVML polled every ~2 ms during the timed region)
+# clocks (NVML polled every ~1 ms during the timed region)
 # --------------------------------------------------------------------------------
 
 class ClockSampler:
@@ -147,7 +147,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv is not None:
