@@ -848,8 +848,9 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
     constexpr int NWP = CF_THREADS / 32;
     __shared__ unsigned long long s_cnt[NWP], s_base[NWP], s_start[NWP];
     __shared__ uint32_t s_ids[CAP3_STAGE];
-    const int c = blockIdx.x, t = cap3_table(a, c);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x;
+    const int t = __shfl_sync(DS_FULL_MASK, lane == 0 ? cap3_table(a, c) : 0, 0);  // one search per warp
     const bool last = c == a.chunk_off[t + 1] - 1;  // this table's last chunk
     uint32_t iv[C3_WPT], uv[C3_WPT];
     int64_t w0, wend;
@@ -894,15 +895,26 @@ __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a)
             *a.ticket = 0u;
         }
     }
-    unsigned long long wbase = 0, tot = 0, b = 0, start = 0;
+    // lane k < NWP holds warp k's values; shuffles give every lane the
+    // exclusive prefix of its warp and the CTA totals
+    const unsigned long long mc = lane < NWP ? s_cnt[lane] : 0ull;
+    unsigned long long b = lane < NWP ? s_base[lane] : 0ull;
+    unsigned long long start = lane < NWP ? s_start[lane] : 0ull;
+    unsigned long long incl = mc;
 #pragma unroll
-    for (int k = 0; k < NWP; k++) {
-        const unsigned long long sw = s_cnt[k];
-        wbase += k < wid ? sw : 0ull;
-        tot += sw;
-        b += s_base[k];
-        start += s_start[k];
+    for (int o = 1; o < NWP; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(DS_FULL_MASK, incl, o);
+        if (lane >= o) incl += y;
     }
+#pragma unroll
+    for (int o = NWP / 2; o > 0; o >>= 1) {
+        b += __shfl_xor_sync(DS_FULL_MASK, b, o);
+        start += __shfl_xor_sync(DS_FULL_MASK, start, o);
+    }
+    b = __shfl_sync(DS_FULL_MASK, b, 0);  // lanes >= NWP reduced zeros
+    start = __shfl_sync(DS_FULL_MASK, start, 0);
+    const unsigned long long tot = __shfl_sync(DS_FULL_MASK, incl, NWP - 1);
+    const unsigned long long wbase = __shfl_sync(DS_FULL_MASK, incl - mc, wid);
     const unsigned long long excl = wbase + x - p;
     const int64_t crow0 = (w0 - threadIdx.x * C3_WPT - a.word_off[t]) * 32;  // chunk's first row
     const unsigned lrow0 = threadIdx.x * C3_WPT * 32;                         // thread's first row
