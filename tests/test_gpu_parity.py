@@ -456,16 +456,17 @@ def test_mark_packed_mixed_widths(ds):
     """Bit-packed and u8 / u16 segments of one stream, every table kind, Zipf
     repeats and ragged lengths: the interval sets equal the unique ids."""
     rng = np.random.default_rng(21)
-    rows = {0: 1, 1: 200, 2: 256, 3: 257, 4: 16352, 5: 40_000, 6: 65_536, 7: 65_537, 8: 12_000_000}
+    rows = {0: 1, 1: 200, 2: 256, 3: 257, 4: 16352, 5: 40_000, 6: 65_536, 7: 65_537, 8: 12_000_000,
+            9: 20_000_000}
     look = {}
     for t, r in rows.items():
         n = int(rng.integers(0, 30_000))
         hot = rng.integers(0, r, 4)
         look[t] = np.where(rng.random(n) < 0.6, hot[rng.integers(0, 4, n)], rng.integers(0, r, n))
     st = ds.LookupStream.pack(look, rows)
-    # bit-packed (4, 12, 20, 24 bits) and plain u8 / u16 segments
-    assert [ds.lookup_width(r) for r in rows.values()] == [4, 8, 8, 12, 16, 16, 16, 20, 24]
-    assert st.seg_width.tolist() == [4, 8, 8, 12, 16, 16, 16, 20, 24]
+    # bit-packed (4, 12, 20, 24, 28 bits) and plain u8 / u16 segments
+    assert [ds.lookup_width(r) for r in rows.values()] == [4, 8, 8, 12, 16, 16, 16, 20, 24, 28]
+    assert st.seg_width.tolist() == [4, 8, 8, 12, 16, 16, 16, 20, 24, 28]
     tr = ds.ModelTracker(rows)
     tr.mark_packed(st.to(tr.device))
     view = tr.capture()
@@ -513,3 +514,25 @@ def test_capture_into_matches_capture(ds, scope):
             assert np.array_equal(h[off:off + c[k]], want[t]), (phase, t)
             off += c[k]
         assert c[len(rows)] == off
+
+
+def test_restore_mixed_dims_and_bitwidths_vs_oracle(ds, O):
+    """One payload whose sections differ in dim (one restore launch per run of
+    equal (dim, bitwidth, aux)); full and incremental; against the oracle's
+    apply_section."""
+    rng = np.random.default_rng(17)
+    shapes = {0: (3000, 16), 1: (500, 8), 2: (2000, 16), 3: (70, 130)}
+    vals = {t: rng.standard_normal(sh).astype(np.float32) for t, sh in shapes.items()}
+    for kind in ("full", "incremental"):
+        for bw in (None, 3, 8):
+            sel = {t: np.sort(rng.choice(sh[0], sh[0] // 3, replace=False)) for t, sh in shapes.items()}
+            blob, _, _ = O.build_shard_payload({t: (v, None) for t, v in vals.items()}, kind,
+                                               sel if kind == "incremental" else None, bw,
+                                               sorted(shapes))
+            got = ds.restore_chain([(kind, [blob])], shapes)
+            for t, (r, dim) in shapes.items():
+                want = np.zeros((r, dim), np.float32)
+                for tid, sec in O.split_sections(blob, kind == "incremental"):
+                    if tid == t:
+                        O.apply_section(sec, kind == "incremental", want)
+                assert np.array_equal(u32(got.tables[t].values.cpu().numpy()), u32(want)), (kind, bw, t)
