@@ -475,6 +475,24 @@ def run_ours(args):
                                "peak": peak_ops / 1e9, "frac": ops / t_write / peak_ops,
                                "evaluations_per_row": E}
 
+    # ---- the store's payload checksum on device (not in the metric) ---------------------
+    # (store.py:46-47 zlib.crc32 of every shard payload)
+    crc = None
+    if nbytes > 0:
+        from paper_2010_08679_b200.payload import crc32 as ds_crc32
+        crc_out = torch.empty(1, dtype=torch.int32, device=dev)
+        for _ in range(3):
+            ds_crc32(ck.payload, nbytes, out=crc_out)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(10):
+            ds_crc32(ck.payload, nbytes, out=crc_out)
+        c1.record()
+        torch.cuda.synchronize()
+        tc = c0.elapsed_time(c1) / 10 / 1e3
+        crc = {"ms": tc * 1e3, "bytes": int(nbytes), "GB/s": nbytes / tc / 1e9,
+               "note": "zlib.crc32 of the step's payload on device (L2-warm), outside the metric"}
+
     # ---- e2e through the public API with host buffers --------------------------------
     # The public pipeline API (paper_2010_08679_b200.pipeline): each step's
     # lookups come from pinned host memory (H2D) and each step's payload goes
@@ -521,7 +539,7 @@ def run_ours(args):
             "config": dict(workload_desc(w), dirty_rows_per_step=dirty_all,
                            parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch),
             "rows_per_s": dirty_all * K / elapsed,
-            "roofline": roofline, "phases": phases,
+            "roofline": roofline, "phases": phases, "payload_crc32": crc,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             # per step: mark_tma 1 + cap3 count/scan/emit 3 + layout/writer/err_reduce 3
             "gpu_launches": K * 7,

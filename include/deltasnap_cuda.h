@@ -237,6 +237,19 @@ DS_API int ds_restore_payload(const uint8_t *payload, const ds_restore_sec *secs
                               void *stream);
 
 /* ------------------------------------------------------------------ */
+/* Payload checksum (store.py:46-47 checksum())      */
+/* ------------------------------------------------------------------ */
+
+/* CRC-32 (IEEE, = zlib.crc32) of n device bytes into *out (device uint32),
+ * asynchronously, one launch: 32 KB chunks per CTA; each chunk shifts its CRC
+ * by the bytes after it with precomputed GF(2) operators and xors it into
+ * *out.  The workspace argument is reserved (may be NULL;
+ * ds_crc32_workspace_size returns a small constant). */
+DS_API size_t ds_crc32_workspace_size(int64_t n);
+DS_API int ds_crc32(const uint8_t *data, int64_t n, uint32_t *out, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Row-matrix codec entry points (quant.py API mirror)                  */
 /* ------------------------------------------------------------------ */
 

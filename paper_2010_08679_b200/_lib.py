@@ -108,6 +108,8 @@ _SIGNATURES = {
     "ds_restore_section": (_I, [_P, _I64, _I64, _I, _I, _I, _I64, _I64, _I64, _P, _I64, _P, _P,
                                 _P, _P]),
     "ds_restore_payload": (_I, [_P, _P, _I, _I64, _I, _I, _I, _P, _P]),
+    "ds_crc32_workspace_size": (_SZ, [_I64]),
+    "ds_crc32": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "ds_quantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),
     "ds_dequantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P, _P]),
     "ds_reconstruction_errors": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),

@@ -536,3 +536,25 @@ def test_restore_mixed_dims_and_bitwidths_vs_oracle(ds, O):
                     if tid == t:
                         O.apply_section(sec, kind == "incremental", want)
                 assert np.array_equal(u32(got.tables[t].values.cpu().numpy()), u32(want)), (kind, bw, t)
+
+
+# --- payload checksum (store.py:46-47) ---------------------------------------------
+
+@pytest.mark.parametrize("n", (0, 1, 3, 4, 5, 127, 128, 129, 4095, 32767, 32768, 32769, 65536,
+                               1_000_003, 20_000_000))
+def test_crc32_matches_zlib(ds, n):
+    import zlib
+    rng = np.random.default_rng(n)
+    b = rng.integers(0, 256, n, dtype=np.uint8)
+    t = torch.from_numpy(b).cuda()
+    assert ds.payload.crc32(t) == zlib.crc32(b.tobytes()) & 0xFFFFFFFF
+    if n > 1:  # unaligned start, prefix length
+        assert ds.payload.crc32(t[1:], n - 1) == zlib.crc32(b[1:].tobytes()) & 0xFFFFFFFF
+
+
+def test_crc32_of_a_payload(ds, O):
+    import zlib
+    rng = np.random.default_rng(3)
+    tabs = {t: (rng.standard_normal((2000, 16)).astype(np.float32), None) for t in range(3)}
+    blob, _, _ = O.build_shard_payload(tabs, "full", None, 4, [0, 1, 2])
+    assert ds.payload.crc32(blob) == zlib.crc32(blob) & 0xFFFFFFFF
