@@ -237,6 +237,40 @@ DS_API int ds_restore_payload(const uint8_t *payload, const ds_restore_sec *secs
                               void *stream);
 
 /* ------------------------------------------------------------------ */
+/* Training step with tracking folded in (sim.py:140-155)  */
+/* ------------------------------------------------------------------ */
+
+typedef struct {
+    float *values;     /* [rows, ld] fp32 */
+    float *aux;        /* may be NULL: no aux update */
+    uint32_t *words;   /* the table's interval bitmap words (may be NULL: no tracking) */
+    int64_t ld;
+    int64_t rows;
+} ds_train_table;
+
+/* apply_batch for nbatches batches in order: for every table t and batch b,
+ * values[idx] += delta and aux[idx] += delta * delta with np.add.at's
+ * semantics (every index in array order: bit-identical float sums) and the
+ * rows' dirty bits set.  ids/deltas are table-major, then batch order:
+ * segment t * nbatches + b = [seg_off[.], seg_off[. + 1]) of idx (device
+ * int64) and of delta (device float [*, dim]); at most 4096 ids per
+ * segment.  Out-of-range ids set DS_FLAG_BOUNDS and are skipped. */
+DS_API int ds_train_apply(const ds_train_table *tables_host, int ntables, int nbatches, int64_t dim,
+                          const int64_t *idx, const float *delta, const int64_t *seg_off,
+                          uint32_t *flags, void *stream);
+
+/* The same update for a whole interval at once: rows (device int64) holds
+ * every table's ids stably sorted by row (table t at sorted positions
+ * [table_off[t], table_off[t+1]), host array), order[i] the position of the
+ * i-th sorted id in delta ([n, dim] device floats, batch order).  Each row's
+ * updates are then one run in np.add.at order; a warp applies a run with
+ * lanes over elements.  Same results as ds_train_apply over the batches. */
+DS_API int ds_train_apply_sorted(const ds_train_table *tables_host, int ntables,
+                                 const int64_t *table_off_host, int64_t dim, const int64_t *rows,
+                                 const int64_t *order, const float *delta, uint32_t *flags,
+                                 void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Payload checksum (store.py:46-47 checksum())      */
 /* ------------------------------------------------------------------ */
 

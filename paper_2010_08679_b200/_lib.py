@@ -69,6 +69,16 @@ class CkptParams(ctypes.Structure):
     ]
 
 
+class TrainTable(ctypes.Structure):
+    _fields_ = [
+        ("values", ctypes.c_void_p),
+        ("aux", ctypes.c_void_p),
+        ("words", ctypes.c_void_p),
+        ("ld", ctypes.c_int64),
+        ("rows", ctypes.c_int64),
+    ]
+
+
 class RestoreSec(ctypes.Structure):
     _fields_ = [
         ("body_off", ctypes.c_int64),
@@ -108,6 +118,8 @@ _SIGNATURES = {
     "ds_restore_section": (_I, [_P, _I64, _I64, _I, _I, _I, _I64, _I64, _I64, _P, _I64, _P, _P,
                                 _P, _P]),
     "ds_restore_payload": (_I, [_P, _P, _I, _I64, _I, _I, _I, _P, _P]),
+    "ds_train_apply": (_I, [_P, _I, _I, _I64, _P, _P, _P, _P, _P]),
+    "ds_train_apply_sorted": (_I, [_P, _I, _P, _I64, _P, _P, _P, _P, _P]),
     "ds_crc32_workspace_size": (_SZ, [_I64]),
     "ds_crc32": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "ds_quantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),

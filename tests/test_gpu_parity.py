@@ -558,3 +558,41 @@ def test_crc32_of_a_payload(ds, O):
     tabs = {t: (rng.standard_normal((2000, 16)).astype(np.float32), None) for t in range(3)}
     blob, _, _ = O.build_shard_payload(tabs, "full", None, 4, [0, 1, 2])
     assert ds.payload.crc32(blob) == zlib.crc32(blob) & 0xFFFFFFFF
+
+
+# --- training step with tracking folded in (sim.py:140-155) -------------------------
+
+@pytest.mark.parametrize("sorted_runs", (True, False))
+def test_apply_batches_matches_np_add_at(ds, sorted_runs):
+    """values/aux after several batches equal np.add.at's sequential sums bit
+    for bit (repeated rows), and the interval bitmap equals mark()."""
+    from paper_2010_08679_b200.train import apply_packed, pack_batches
+    rng = np.random.default_rng(12)
+    rows, dim = {0: 500, 1: 70_000, 2: 7}, 16
+    vals = {t: rng.standard_normal((r, dim)).astype(np.float32) for t, r in rows.items()}
+    auxs = {t: rng.random((r, dim)).astype(np.float32) for t, r in rows.items()}
+    tabs = {t: ds.DeviceTable(t, torch.from_numpy(vals[t]).cuda(), torch.from_numpy(auxs[t]).cuda())
+            for t in rows}
+    tr, ref_tr = ds.ModelTracker(rows), ds.ModelTracker(rows)
+    batches = []
+    for b in range(4):
+        batch = {}
+        for t, r in rows.items():
+            n = int(rng.integers(1, 4096))
+            hot = rng.integers(0, r, 5)
+            idx = np.where(rng.random(n) < 0.5, hot[rng.integers(0, 5, n)], rng.integers(0, r, n))
+            batch[t] = (idx.astype(np.int64), (rng.standard_normal((n, dim)) * 0.01).astype(np.float32))
+        batches.append(batch)
+    apply_packed(tabs, pack_batches(tabs, batches[:1]), tracker=tr, sorted_runs=sorted_runs)
+    apply_packed(tabs, pack_batches(tabs, batches[1:]), tracker=tr, sorted_runs=sorted_runs)
+    for batch in batches:
+        for t in sorted(batch):
+            idx, delta = batch[t]
+            np.add.at(vals[t], idx, delta)
+            np.add.at(auxs[t], idx, delta * delta)
+            ref_tr.mark(t, idx)
+    view, ref = tr.capture(), ref_tr.capture()
+    for t in rows:
+        assert np.array_equal(u32(tabs[t].values.cpu().numpy()), u32(vals[t])), t
+        assert np.array_equal(u32(tabs[t].aux.cpu().numpy()), u32(auxs[t])), t
+        assert np.array_equal(view.interval_rows[t], ref.interval_rows[t]), t
