@@ -57,6 +57,7 @@ from .engine import (
     build_shard_payload,
     restore,
     restore_chain,
+    stage_chain,
 )
 
 __version__ = "0.1.0"

@@ -367,23 +367,87 @@ def restore_chain(chain: list, table_shapes: dict, *, aux: bool = False, device=
     for kind, payloads in chain:
         inc = kind == INCREMENTAL
         for data in payloads:
-            apply_payload(data, inc, tables, baseline if inc else None, device=dev)
+            # (host bytes, device copy) pairs come from stage_chain
+            host, dbuf = data if isinstance(data, tuple) else (data, None)
+            apply_payload(host, inc, tables, baseline if inc else None, device=dev, device_buf=dbuf)
     return RestoredTables(tables=tables, tracker=tracker)
 
 
+def stage_chain(chain: list, checksums: list | None = None, device=None) -> list:
+    """Move a chain's payloads to the device and verify them there before
+    anything is applied (store.py:488-507 verify).
+
+    chain: [(kind, [payload bytes, ...]), ...]; checksums: matching
+    [[crc32, ...], ...] (manifest ObjectEntry.crc32) or None.  Each payload
+    is H2D-copied from pinned memory on a copy stream while the previous one
+    is checksummed on the device (ds_crc32); one sync at the end compares
+    every CRC and raises IntegrityError for the first mismatch, like the
+    reference.  Returns the chain with (bytes, device buffer) pairs for
+    restore_chain.
+    """
+    from .payload import crc32 as dev_crc32
+
+    dev = device_of(device)
+    main = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    staged, crcs, want = [], [], []
+    for ci, (kind, payloads) in enumerate(chain):
+        out = []
+        for pi, data in enumerate(payloads):
+            buf = np.frombuffer(data, dtype=np.uint8)
+            dbuf = torch.empty(buf.size + 16, dtype=torch.uint8, device=dev)
+            if buf.size:
+                host = torch.from_numpy(buf.copy()).pin_memory()
+                with torch.cuda.stream(copy):
+                    dbuf[:buf.size].copy_(host, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                main.wait_event(ev)  # the CRC of this payload runs after its copy
+            if checksums is not None:
+                c = torch.zeros(1, dtype=torch.int32, device=dev)
+                dev_crc32(dbuf, buf.size, out=c)
+                crcs.append(c)
+                want.append((checksums[ci][pi], f"payload {pi} of chain entry {ci}"))
+            out.append((data, dbuf))
+        staged.append((kind, out))
+    if crcs:
+        got = torch.cat(crcs).cpu().numpy().astype(np.uint32)
+        for g, (w, what) in zip(got, want):
+            if int(g) != (int(w) & 0xFFFFFFFF):
+                raise IntegrityError(f"checksum mismatch for {what}")
+    return staged
+
+
 def restore(cstore, *, fallback: bool = False, checkpoint_id: int | None = None,
-            device=None) -> RestoredTables:
+            device=None, verify_on_device: bool = False) -> RestoredTables:
     """restore() over a reference-compatible CheckpointStore (engine.py:515-535).
 
-    Chain resolution and CRC verification are the store's (host, out of
-    scope); decoding and scattering run on the GPU.
+    Chain resolution is the store's (host); decoding and scattering run on
+    the GPU.  verify_on_device: the shard payloads' CRC32 checks of
+    store.verify (store.py:488-507) run on the device after the H2D copy
+    (stage_chain) instead of on the host.
     """
     def restore_at(cid):
-        chain = cstore.verify_chain(cid)
+        if verify_on_device:
+            # presence and sizes on the host, checksums on the device
+            chain = cstore.resolve_chain(cid)
+            for m in chain:
+                for e in list(m.shards.values()) + [m.dense]:
+                    try:
+                        n = len(cstore.store.get(e.key))
+                    except KeyError:
+                        raise IntegrityError(f"missing object {e.key!r}") from None
+                    if n != e.nbytes:
+                        raise IntegrityError(f"size mismatch for {e.key!r}: {n} != {e.nbytes}")
+        else:
+            chain = cstore.verify_chain(cid)
         target = chain[-1]
         shapes = {tid: (info.rows, info.dim) for tid, info in target.tables.items()}
         plan = [(m.kind, [cstore.store.get(e.key) for _, e in sorted(m.shards.items())])
                 for m in chain]
+        if verify_on_device:
+            sums = [[e.crc32 for _, e in sorted(m.shards.items())] for m in chain]
+            plan = stage_chain(plan, sums, device=device)
         out = restore_chain(plan, shapes, aux=bool(target.aux), device=device)
         out.chain_ids = [m.checkpoint_id for m in chain]
         out.manifest = target

@@ -596,3 +596,26 @@ def test_apply_batches_matches_np_add_at(ds, sorted_runs):
         assert np.array_equal(u32(tabs[t].values.cpu().numpy()), u32(vals[t])), t
         assert np.array_equal(u32(tabs[t].aux.cpu().numpy()), u32(auxs[t])), t
         assert np.array_equal(view.interval_rows[t], ref.interval_rows[t]), t
+
+
+def test_stage_chain_verifies_on_device(ds, golden):
+    """Restore-side checksums on the device (store.py:488-507): a good chain
+    restores exactly like restore_chain; one flipped byte raises
+    IntegrityError before any table is touched."""
+    import zlib
+    g = golden("restore")
+    tag = "bw3"
+    rows, d = g[f"{tag}_values_t0"].shape
+    chain = [(str(g[f"{tag}_kind{i}"]), [g[f"{tag}_m{i}_s{s}"].tobytes() for s in range(2)])
+             for i in range(int(g[f"{tag}_nchain"]))]
+    sums = [[zlib.crc32(p) for p in ps] for _, ps in chain]
+    shapes = {0: (rows, d), 1: (rows, d)}
+    out = ds.restore_chain(ds.stage_chain(chain, sums), shapes, aux=True)
+    for t in range(2):
+        assert np.array_equal(u32(out.tables[t].values.cpu().numpy()), u32(g[f"{tag}_values_t{t}"]))
+    bad = [(k, list(ps)) for k, ps in chain]
+    b = bytearray(bad[-1][1][0])
+    b[len(b) // 2] ^= 0x40
+    bad[-1][1][0] = bytes(b)
+    with pytest.raises(ds.IntegrityError):
+        ds.stage_chain(bad, sums)
