@@ -475,6 +475,31 @@ def run_ours(args):
                                "peak": peak_ops / 1e9, "frac": ops / t_write / peak_ops,
                                "evaluations_per_row": E}
 
+    # ---- stall-window staging (not in the metric) -------------------
+    # the stall a training loop sees: K2 + the dirty-row gather; K3 then runs
+    # from the staged copy on a side stream
+    staged = None
+    if True:
+        cap = int(dirty_rank * 1.25) + 1024
+        sst, stot = [], []
+        for k in range(max(3, min(K, 20)) + 3):
+            ck.mark(stream)
+            flush.fill_(k & 0xFF)
+            s0, s2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            stall_end = ck.checkpoint(staged_rows=cap)
+            ck.wait()
+            s2.record()
+            torch.cuda.synchronize()
+            if k >= 3:
+                sst.append(s0.elapsed_time(stall_end))
+                stot.append(s0.elapsed_time(s2))
+        _ = ck.fetch()
+        staged = {"stall_ms": float(np.median(sst)), "checkpoint_ms": float(np.median(stot)),
+                  "direct_stall_ms": (t_cap + t_write) * 1e3,
+                  "note": "stall = capture + dirty-row gather; K3 then runs from the copy on a "
+                          "side stream (the direct path stalls for capture + K3)"}
+
     # ---- the store's payload checksum on device (not in the metric) ---------------------
     # (store.py:46-47 zlib.crc32 of every shard payload)
     crc = None
@@ -539,7 +564,7 @@ def run_ours(args):
             "config": dict(workload_desc(w), dirty_rows_per_step=dirty_all,
                            parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch),
             "rows_per_s": dirty_all * K / elapsed,
-            "roofline": roofline, "phases": phases, "payload_crc32": crc,
+            "roofline": roofline, "phases": phases, "payload_crc32": crc, "staged": staged,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             # per step: mark_tma 1 + cap3 count/scan/emit 3 + layout/writer/err_reduce 3
             "gpu_launches": K * 7,

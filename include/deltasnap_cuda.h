@@ -173,6 +173,9 @@ typedef struct {
     int ids_local;      /* 1: ids are table-local rows (capture output); the record
                            carries row_base + id */
     unsigned long long *stats; /* optional device counters (DS_STAT_*), may be NULL */
+    const float *staged;       /* optional: rows already gathered by ds_stage_rows (record i
+                                  of the packed id order at staged[i * dim]); the tables are
+                                  then only used for bounds, row_base and dims */
 } ds_ckpt_params;
 
 /* Counters of the certified fast path (diagnostics). */
@@ -195,6 +198,16 @@ DS_API int ds_write_payload(const ds_table_desc *tables_host, int ntables, const
                      const int64_t *ids, const int64_t *counts, uint8_t *payload,
                      int64_t payload_capacity, int64_t *sec_off, double *err_sum,
                      uint32_t *flags, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Stall-window staging: gather the dirty rows named by
+ * ids (table-local, packed per table in table order, counts[ntables] =
+ * total, capture_into's layout) into staged[k * dim] so the writer can run
+ * from the copy (ds_ckpt_params.staged) while training updates the tables.
+ * max_rows is the staging capacity in rows; a larger total sets
+ * DS_FLAG_CAPACITY (the total stays on the device). */
+DS_API int ds_stage_rows(const ds_table_desc *tables_host, int ntables, const int64_t *ids,
+                         const int64_t *counts, int64_t max_rows, float *staged, uint32_t *flags,
+                         void *stream);
 
 /* Upper bound of the payload bytes for the given row counts (host math). */
 DS_API int64_t ds_record_size(int64_t dim, int bitwidth, int aux, int incremental);

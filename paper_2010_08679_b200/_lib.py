@@ -66,6 +66,7 @@ class CkptParams(ctypes.Structure):
         ("ids_packed", ctypes.c_int),
         ("ids_local", ctypes.c_int),
         ("stats", ctypes.c_void_p),
+        ("staged", ctypes.c_void_p),
     ]
 
 
@@ -115,6 +116,7 @@ _SIGNATURES = {
     "ds_writer_workspace_size": (_SZ, [_I, _I64, _I64]),
     "ds_write_payload": (_I, [_P, _I, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
     "ds_record_size": (_I64, [_I64, _I, _I, _I]),
+    "ds_stage_rows": (_I, [_P, _I, _P, _P, _I64, _P, _P, _P]),
     "ds_restore_section": (_I, [_P, _I64, _I64, _I, _I, _I, _I64, _I64, _I64, _P, _I64, _P, _P,
                                 _P, _P]),
     "ds_restore_payload": (_I, [_P, _P, _I, _I64, _I, _I, _I, _P, _P]),

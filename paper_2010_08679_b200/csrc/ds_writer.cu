@@ -43,6 +43,94 @@ static int64_t warp_tiles(int64_t rows, int ntables, int64_t dim) {
     return rows / tr + ntables + 1;
 }
 
+// ---------------------------------------------------------------------------
+// stall-window staging: staged[k] = values_t[ids[k]] for the packed ids
+// ---------------------------------------------------------------------------
+struct StageArgs {
+    ds_table_desc t[DS_MAX_TABLES];
+    const int64_t *ids;
+    const int64_t *counts;
+    float *staged;
+    uint32_t *flags;
+    int64_t max_rows;
+    int ntables, dim, vec;
+};
+
+__global__ void __launch_bounds__(256) stage_rows_kernel(const StageArgs a) {
+    __shared__ int64_t s_off[DS_MAX_TABLES + 1];
+    const int nt = a.ntables;
+    if (threadIdx.x < 32) {  // packed id offsets: one warp scan over the counts
+        const int lane = threadIdx.x;
+        int64_t base = 0;
+        for (int b = 0; b < nt; b += 32) {
+            const int64_t n = b + lane < nt ? a.counts[b + lane] : 0;
+            int64_t x = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(DS_FULL_MASK, x, o);
+                if (lane >= o) x += y;
+            }
+            if (b + lane < nt) s_off[b + lane] = base + x - n;
+            base += __shfl_sync(DS_FULL_MASK, x, 31);
+        }
+        if (lane == 0) s_off[nt] = base;
+    }
+    __syncthreads();
+    int64_t total = s_off[nt];
+    if (total > a.max_rows) {  // the staging buffer is too small: flagged, capped
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(a.flags, DS_FLAG_CAPACITY);
+        total = a.max_rows;
+    }
+    const int d = a.dim;
+    // lanes per row: one float4 each (or one float) up to a warp
+    const int per = a.vec ? (d >> 2) : d;
+    const int gl = per >= 32 ? 32 : (per >= 16 ? 16 : (per >= 8 ? 8 : (per >= 4 ? 4 : (per >= 2 ? 2 : 1))));
+    const int lane = threadIdx.x & 31, lig = lane % gl;
+    const int64_t rows_per_step = ((int64_t)gridDim.x * blockDim.x) / gl;
+    bool bad = false;
+    constexpr int U = 4;  // rows in flight per lane group
+    for (int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / gl; k0 < total;
+         k0 += U * rows_per_step) {
+        const float *src[U];
+        int64_t kk[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t k = k0 + u * rows_per_step;
+            kk[u] = k;
+            src[u] = nullptr;
+            if (k < total) {
+                int lo = 0, hi = nt - 1;  // table of packed position k
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_off[mid] <= k) lo = mid;
+                    else hi = mid - 1;
+                }
+                const ds_table_desc &td = a.t[lo];
+                const int64_t id = a.ids[k];
+                if (id < 0 || id >= td.rows) bad = true;
+                else src[u] = td.values + id * td.ld;
+            }
+        }
+        if (a.vec) {
+            for (int c = lig; c < per; c += gl) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (src[u]) v[u] = __ldg(reinterpret_cast<const float4 *>(src[u]) + c);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (src[u]) __stcs(reinterpret_cast<float4 *>(a.staged + kk[u] * (int64_t)d) + c, v[u]);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                if (src[u])
+                    for (int e = lig; e < d; e += gl) a.staged[kk[u] * (int64_t)d + e] = __ldg(src[u] + e);
+        }
+    }
+    if (__any_sync(DS_FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flags, DS_FLAG_BOUNDS);
+}
+
 }  // namespace ds
 
 using namespace ds;
@@ -62,6 +150,10 @@ extern "C" size_t ds_writer_workspace_size(int ntables, int64_t max_rows, int64_
     // done counter + 4096 error partials + one fixup mask word per warp-tile
     int64_t tiles = warp_tiles(max_rows > 0 ? max_rows : 0, ntables, dim > 0 ? dim : 1);
     return ws_head_bytes() + (size_t)tiles * sizeof(uint32_t) + 256;
+}
+
+static int mode_of(const ds_ckpt_params *p) {
+    return p->bitwidth == 0 ? 0 : (p->adaptive_bins > 0 ? 2 : 1);
 }
 
 extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
@@ -125,6 +217,10 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     a.capacity = capacity;
     a.flags = flags;
     a.stats = p->stats;
+    a.staged = p->staged;
+    if (p->staged && (!p->incremental || !p->ids_packed || p->aux || (mode_of(p) == 2 && DS_GREEDY_CTA)))
+        return host::fail(DS_ERR_ARG, "ds_write_payload: staged rows need an incremental "
+                                      "checkpoint with packed ids and no aux");
 
     const int mode = bw == 0 ? 0 : (p->adaptive_bins > 0 ? 2 : 1);
     Cfg c = pick_cfg(d, vec4, mode);
@@ -175,4 +271,36 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     // one launch: layout, records, exact fixups and the error sum
     fn<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(a);
     return host::check_launch("ds_write_payload");
+}
+
+extern "C" int ds_stage_rows(const ds_table_desc *tables_host, int ntables, const int64_t *ids,
+                             const int64_t *counts, int64_t max_rows, float *staged, uint32_t *flags,
+                             void *stream) {
+    if (ntables < 1 || ntables > DS_MAX_TABLES) return host::fail(DS_ERR_ARG, "ds_stage_rows: ntables");
+    if (!tables_host || !counts || !flags) return host::fail(DS_ERR_ARG, "ds_stage_rows: null pointer");
+    if (max_rows <= 0) return DS_OK;
+    if (!ids || !staged) return host::fail(DS_ERR_ARG, "ds_stage_rows: null ids / staged");
+    StageArgs a;
+    a.ntables = ntables;
+    a.ids = ids;
+    a.counts = counts;
+    a.staged = staged;
+    a.flags = flags;
+    a.max_rows = max_rows;
+    a.dim = (int)tables_host[0].dim;
+    a.vec = a.dim % 4 == 0 && (reinterpret_cast<uintptr_t>(staged) & 15) == 0;
+    for (int t = 0; t < ntables; t++) {
+        if ((int)tables_host[t].dim != a.dim)
+            return host::fail(DS_ERR_SHAPE, "ds_stage_rows: tables of one call share dim");
+        a.t[t] = tables_host[t];
+        if (tables_host[t].ld % 4 || (reinterpret_cast<uintptr_t>(tables_host[t].values) & 15)) a.vec = 0;
+    }
+    const int per = a.vec ? a.dim / 4 : a.dim;
+    const int gl = per >= 32 ? 32 : (per >= 16 ? 16 : (per >= 8 ? 8 : (per >= 4 ? 4 : (per >= 2 ? 2 : 1))));
+    int64_t blocks = (max_rows * gl + 255) / 256;
+    const int64_t cap = (int64_t)host::sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    stage_rows_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a);
+    return host::check_launch("ds_stage_rows");
 }

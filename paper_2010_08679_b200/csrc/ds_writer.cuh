@@ -54,6 +54,7 @@ struct WriterArgs {
     uint32_t *fix_mask;    // MODE 1: per warp-tile mask of rows for the fixup pass
     uint32_t *flags;
     unsigned long long *stats;
+    const float *staged;  // rows gathered by ds_stage_rows (read record i of the packed order)
 };
 
 // ---------------------------------------------------------------------------
@@ -592,7 +593,10 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
         }
     }
     float x[EPL];
-    if (mine) load_row<G, C, VEC>(td.values + local * td.ld, d, lig, x, 0.f);
+    if (mine)
+        load_row<G, C, VEC>(a.staged ? a.staged + (s_sched[2 * nt + 1 + t] + i0 + slot) * (int64_t)d
+                                     : td.values + local * td.ld,
+                            d, lig, x, 0.f);
     else
 #pragma unroll
         for (int k = 0; k < EPL; k++) x[k] = 0.f;
@@ -786,7 +790,9 @@ __global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRI
             const int64_t loc = __shfl_sync(DS_FULL_MASK, T.loc, r);
             if (T.ok && r < T.nrow && loc >= 0) {
                 const ds_table_desc &td = a.t[T.t];
-                const float *src = td.values + loc * td.ld;
+                // staged: record i0 + r of table t sits at its packed position
+                const float *src = a.staged ? a.staged + (s_sched[2 * nt + 1 + T.t] + T.i0 + r) * (int64_t)d
+                                            : td.values + loc * td.ld;
                 float *dst = ring + st * (chunk_b / 4) + slot * d;
                 float *sbase = ring + st * (chunk_b / 4);
 #pragma unroll

@@ -19,6 +19,7 @@ NaN/Inf rows raise DataError in every quantized mode (the reference's naive
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 
@@ -60,6 +61,10 @@ class DeviceTable:
     @property
     def dim(self) -> int:
         return self.values.shape[1]
+
+
+def _nullctx():
+    return contextlib.nullcontext()
 
 
 def adaptive_for(bitwidth: int, overrides) -> AdaptiveConfig | None:
@@ -144,7 +149,7 @@ class ShardWriter:
 
     def write(self, payload: torch.Tensor, ids: torch.Tensor | None = None,
               counts: torch.Tensor | None = None, ids_offsets=None, *, local_ids: bool = False,
-              stream=None) -> None:
+              stream=None, staged: torch.Tensor | None = None) -> None:
         """Launch layout + writer (+ error reduction).
 
         Incremental when `ids` is given: ids concatenates every table's row
@@ -158,16 +163,30 @@ class ShardWriter:
         self.params.incremental = int(incremental)
         self.params.ids_packed = int(incremental and ids_offsets is None)
         self.params.ids_local = int(local_ids)
+        # rows gathered by stage_rows (packed id order) instead of the live tables
+        self.params.staged = staged.data_ptr() if staged is not None else None
         if incremental and ids_offsets is not None:
             for k in range(len(self.tables)):
                 self._descs[k].ids_off = int(ids_offsets[k])
-        self.flags.zero_()
+        if staged is None:  # (stage_rows cleared the flags for a staged write)
+            self.flags.zero_()
         _lib.check(self.L.ds_write_payload(
             ctypes.cast(self._descs, ctypes.c_void_p), len(self.tables), ctypes.byref(self.params),
             ids.data_ptr() if incremental else None,
             counts.data_ptr() if incremental else None, payload.data_ptr(), payload.numel(),
             self.sec_off.data_ptr(), self.err.data_ptr(), self.flags.data_ptr(),
             self._ws.data_ptr(), self._ws.numel(), _lib.stream_handle(stream)), "write_payload")
+
+    def stage_rows(self, ids: torch.Tensor, counts: torch.Tensor, staged: torch.Tensor,
+                   stream=None) -> None:
+        """Gather the dirty rows (packed table-local ids, counts with the total
+        at [ntables]) into staged [capacity, dim]."""
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            self.flags.zero_()
+        _lib.check(self.L.ds_stage_rows(
+            ctypes.cast(self._descs, ctypes.c_void_p), len(self.tables), ids.data_ptr(),
+            counts.data_ptr(), staged.shape[0], staged.data_ptr(), self.flags.data_ptr(),
+            _lib.stream_handle(stream)), "stage_rows")
 
     def finish(self) -> tuple:
         """Synchronise; raise flagged errors; (total payload bytes, err_sum)."""

@@ -58,6 +58,9 @@ class ShardedCheckpointer:
         self.payload = torch.empty(self.capacity + 16, dtype=torch.uint8, device=self.device)
         self._seg_cache = None
         self._comm = torch.cuda.Stream(self.device) if world_size > 1 else None
+        self._stage_buf = None
+        self._side = None
+        self._pending = None
 
     # -- the device-side step ---------------------------------------------------
 
@@ -69,13 +72,23 @@ class ShardedCheckpointer:
         else:
             self.tracker.mark_batch(idx, seg_off, seg_tables)
 
-    def checkpoint(self) -> None:
+    def checkpoint(self, staged_rows: int = 0):
         """K2, then K3 overlapped with the count all_gather, asynchronous on the
         current stream.  Only the host-side assembly needs the global counts, so
         the collective runs on a side stream while the writer runs; the
-        current stream joins it before returning (step time includes it)."""
+        current stream joins it before returning (step time includes it).
+
+        staged_rows > 0 (stall-window staging): the dirty
+        rows are gathered into a staging buffer of that many rows on the
+        current stream, and K3 runs from the copy on a side stream; the
+        returned event marks the end of the stall -- training may update the
+        tables once the current stream passes it.  fetch()/layout() wait for
+        the side stream.  (A dirty count above staged_rows raises at fetch.)
+        """
         fold = 1
         self.counts = self.tracker.capture_into(self.ids, None, fold=fold, scope=self.scope)
+        if staged_rows > 0:
+            return self._checkpoint_staged(staged_rows)
         if self.world > 1:
             main = torch.cuda.current_stream(self.device)
             self._comm.wait_stream(main)
@@ -86,6 +99,30 @@ class ShardedCheckpointer:
         else:
             self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
 
+    def _checkpoint_staged(self, cap: int):
+        main = torch.cuda.current_stream(self.device)
+        if self._stage_buf is None or self._stage_buf.shape[0] < cap:
+            self._stage_buf = torch.empty((cap, self.tables[0].dim), dtype=torch.float32,
+                                          device=self.device)
+            self._side = torch.cuda.Stream(self.device)
+        self.writer.stage_rows(self.ids, self.counts, self._stage_buf[:cap])
+        stall_end = torch.cuda.Event(enable_timing=True)
+        stall_end.record(main)
+        self._side.wait_event(stall_end)
+        with torch.cuda.stream(self._side):
+            if self.world > 1:
+                gather_counts(self.counts, self.world, self.group, out=self.all_counts)
+            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True,
+                              staged=self._stage_buf[:cap])
+        self._pending = self._side
+        return stall_end
+
+    def wait(self) -> None:
+        """Join a staged checkpoint's side stream into the current stream."""
+        if self._pending is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self._pending)
+            self._pending = None
+
     def step(self, idx, seg_off=None, seg_tables=None) -> None:
         self.mark(idx, seg_off, seg_tables)
         self.checkpoint()
@@ -95,6 +132,7 @@ class ShardedCheckpointer:
     def layout(self):
         """(local payload bytes, per-table local counts, per-table totals,
         section offsets, this rank's run offsets) after a sync; see shard_layout."""
+        self.wait()
         counts_all = self.all_counts.view(self.world, self.nt + 1).cpu().numpy() \
             if self.world > 1 else self.counts.view(1, self.nt + 1).cpu().numpy()
         per_table, sec_off, run_off = shard_layout(counts_all[:, :self.nt], self.rank, self.rec)
@@ -106,6 +144,7 @@ class ShardedCheckpointer:
 
     def fetch(self, out: torch.Tensor | None = None, stream=None):
         """D2H of this rank's bytes into pinned memory; raises flagged errors."""
+        self.wait()
         _lib.raise_flags(int(self.writer.flags.item()), "checkpoint")
         nbytes = int(self.writer.sec_off[-1].item())
         if out is None:

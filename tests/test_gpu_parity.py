@@ -619,3 +619,33 @@ def test_stage_chain_verifies_on_device(ds, golden):
     bad[-1][1][0] = bytes(b)
     with pytest.raises(ds.IntegrityError):
         ds.stage_chain(bad, sums)
+
+
+def test_staged_checkpoint_matches_direct(ds, O):
+    """Stall-window staging: K3 from the gathered copy on a
+    side stream, while the tables are overwritten right after the stall,
+    yields the same payload as the direct path (and the oracle)."""
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    rng = np.random.default_rng(31)
+    rows = {0: 300, 1: 70_000, 2: 2_000_000}
+    for bw in (8, 4, None):
+        vals = {t: rng.standard_normal((r, 16)).astype(np.float32) for t, r in rows.items()}
+        tabs = [ds.DeviceTable(t, torch.from_numpy(vals[t]).cuda()) for t in rows]
+        look = {t: rng.integers(0, r, 30_000) for t, r in rows.items()}
+        ck = ShardedCheckpointer(tabs, bw, device="cuda")
+        ck.mark(ds.LookupStream.pack(look, rows).to(tabs[0].values.device))
+        stall_end = ck.checkpoint(staged_rows=100_000)
+        torch.cuda.current_stream().wait_event(stall_end)
+        for t in tabs:  # "training" resumes: the live tables change
+            t.values.add_(1.0)
+        buf, n = ck.fetch()
+        torch.cuda.synchronize()
+        sel = {t: np.unique(look[t]) for t in rows}
+        ref, _, _ = O.build_shard_payload({t: (vals[t], None) for t in rows}, "incremental", sel, bw,
+                                          sorted(rows))
+        assert bytes(buf[:n].numpy()) == ref, bw
+    # a staging buffer that is too small is reported, not silently truncated
+    ck.mark(ds.LookupStream.pack(look, rows).to(tabs[0].values.device))
+    ck.checkpoint(staged_rows=1000)
+    with pytest.raises(ValueError):
+        ck.fetch()
