@@ -367,6 +367,9 @@ __device__ __forceinline__ void eval_fast(const float (&x)[C * VEC], int d, int 
 // Both candidates of a greedy step in one pass over the row: two independent
 // accumulation chains per element (ILP), one loop over the registers.  Same
 // arithmetic and bounds as two eval_fast calls.
+#ifndef DS_GREEDY_NO_TIES
+#define DS_GREEDY_NO_TIES 0
+#endif
 template <int G, int C, int VEC, bool PAD>
 __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int lig, float loA,
                                            float hiA, float loB, float hiB, int L, float &SA,
@@ -388,8 +391,12 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
         const float vA = __fmul_rn(__fsub_rn(cA, loA), invA);
         const float vB = __fmul_rn(__fsub_rn(cB, loB), invB);
         const float qA = rintf(vA), qB = rintf(vB);
-        rmA = fmaxf(rmA, fabsf(__fsub_rn(vA, qA)));
-        rmB = fmaxf(rmB, fabsf(__fsub_rn(vB, qB)));
+        if (!DS_GREEDY_NO_TIES) {
+            rmA = fmaxf(rmA, fabsf(__fsub_rn(vA, qA)));
+            rmB = fmaxf(rmB, fabsf(__fsub_rn(vB, qB)));
+        } else {
+            rmA = rmB = 1.f;  // always budget for code ties (no per-element tracking)
+        }
         float eA = __fsub_rn(x[k], __fmaf_rn(qA, sA, loA));
         float eB = __fsub_rn(x[k], __fmaf_rn(qB, sB, loB));
         if (PAD) {
