@@ -14,7 +14,7 @@ struct WarpPlan {
 };
 static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c, int mode = 1) {
     const int rpc = 32 / c.G;
-    const int ns = c.G == 1 ? 2 : DS_WRITER_NS;  // writer_stages<G>()
+    const int ns = c.G == 1 ? DS_WRITER_NS1 : DS_WRITER_NS;  // writer_stages<G>()
     auto warp_bytes = [&](int trr) {
         return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) +
                (size_t)ns * ((rpc * d * 4 + 63) & ~63) +
@@ -22,8 +22,9 @@ static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c, int mode = 1) {
     };
     WarpPlan p;
     p.tr = 32;
-    while (warp_bytes(p.tr) * (WT / 32) > 200 * 1024 && p.tr / 2 >= rpc * (ns - 1) && p.tr > 1) p.tr /= 2;
-    p.threads = WT;
+    while (warp_bytes(p.tr) * (DS_WT_WARP / 32) > 200 * 1024 && p.tr / 2 >= rpc * (ns - 1) && p.tr > 1)
+        p.tr /= 2;
+    p.threads = DS_WT_WARP;
     while (warp_bytes(p.tr) * (p.threads / 32) > 200 * 1024 && p.threads > 32) p.threads /= 2;
     p.smem = warp_bytes(p.tr) * (p.threads / 32) + 16;  // + alignment slack
     return p;

@@ -696,14 +696,20 @@ __device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
 #ifndef DS_WRITER_NS
 #define DS_WRITER_NS 3
 #endif
+#ifndef DS_WRITER_NS1
+#define DS_WRITER_NS1 2
+#endif
 template <int G>
-__host__ __device__ constexpr int writer_stages() { return G == 1 ? 2 : DS_WRITER_NS; }
+__host__ __device__ constexpr int writer_stages() { return G == 1 ? DS_WRITER_NS1 : DS_WRITER_NS; }
 
 #ifndef DS_WRITER_MINB_GREEDY
 #define DS_WRITER_MINB_GREEDY 2
 #endif
+#ifndef DS_WT_WARP
+#define DS_WT_WARP WT  // threads per CTA of the warp-pipelined writer
+#endif
 template <int G, int C, int VEC, int MODE, bool PAD>
-__global__ void __launch_bounds__(WT, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
+__global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
     writer_warp_kernel(const WriterArgs a) {
     constexpr int EPL = C * VEC;
     constexpr int RPC = 32 / G;  // rows per chunk
