@@ -649,3 +649,49 @@ def test_staged_checkpoint_matches_direct(ds, O):
     ck.checkpoint(staged_rows=1000)
     with pytest.raises(ValueError):
         ck.fetch()
+
+
+def test_empty_inputs(ds, O):
+    """Empty marks, empty selections, zero-row codec calls, header-only
+    payloads and empty lookup streams behave like the reference."""
+    bm = ds.DirtyBitmap(0, 100)
+    bm.mark(np.zeros(0, np.int64))
+    ids, frac = bm.dirty_rows()
+    assert ids.size == 0 and frac == 0.0 and bm.popcount() == 0
+    tr = ds.ModelTracker({0: 1, 1: 50})
+    view = tr.capture()
+    assert all(view.interval_rows[t].size == 0 for t in (0, 1))
+    x = np.zeros((0, 16), np.float32)
+    lo = hi = np.zeros(0, np.float32)
+    assert ds.quantize_rows(x, lo, hi, 4).shape == (0, 16)
+    assert ds.pack_code_rows(np.zeros((0, 16), np.uint8), 4).shape[0] == 0
+    # header-only payload: every table selected with no rows
+    tabs = {t: (np.ones((10, 16), np.float32), None) for t in range(3)}
+    sel = {t: np.zeros(0, np.int64) for t in range(3)}
+
+    class _T:
+        def __init__(self, t):
+            self.table_id, self.values, self.aux = t, tabs[t][0], None
+
+    class _S:
+        def shard_tables(self, sid):
+            return [_T(t) for t in range(3)]
+
+    class _P:
+        kind, rows, bitwidth = "incremental", sel, 8
+
+    blob, q, err = ds.build_shard_payload(_S(), _P(), 0)
+    ref, q_ref, err_ref = O.build_shard_payload(tabs, "incremental", sel, 8, [0, 1, 2])
+    assert blob == ref and q == q_ref == 0 and err == err_ref == 0.0
+    out = ds.restore_chain([("incremental", [blob])], {t: (10, 16) for t in range(3)})
+    assert all(float(out.tables[t].values.abs().sum()) == 0.0 for t in range(3))
+    # an empty lookup stream and a checkpoint with nothing dirty
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    rows = {0: 10, 1: 100_000}
+    st = ds.LookupStream.pack({0: np.zeros(0, np.int64), 1: np.zeros(0, np.int64)}, rows)
+    dt = [ds.DeviceTable(t, torch.ones((r, 16), device="cuda")) for t, r in rows.items()]
+    ck = ShardedCheckpointer(dt, 8, device="cuda")
+    ck.step(st.to(dt[0].values.device))
+    buf, n = ck.fetch()
+    torch.cuda.synchronize()
+    assert n == 2 * 24  # two headers, no records
