@@ -695,3 +695,37 @@ def test_empty_inputs(ds, O):
     buf, n = ck.fetch()
     torch.cuda.synchronize()
     assert n == 2 * 24  # two headers, no records
+
+
+def test_mark_batch_unaligned_segments(ds):
+    """Segments that do not start on 16 bytes take the grid-stride K1 form."""
+    rng = np.random.default_rng(23)
+    rows = {0: 1000, 1: 300_000, 2: 7}
+    tr = ds.ModelTracker(rows)
+    idx, seg = [], [0]
+    for t, r in rows.items():
+        a = rng.integers(0, r, int(rng.integers(1, 3000)) * 2 + 1)  # odd lengths
+        idx.append(a)
+        seg.append(seg[-1] + a.size)
+    for dtype in (torch.int32, torch.int64):
+        tr.mark_batch(torch.from_numpy(np.concatenate(idx)).to(dtype).cuda(), np.array(seg),
+                      np.array(list(rows)))
+        view = tr.capture()
+        for k, t in enumerate(rows):
+            assert np.array_equal(view.interval_rows[t], np.unique(idx[k])), (dtype, t)
+        tr.reset_interval()
+
+
+@pytest.mark.slow
+def test_capture_beyond_32bit_row_counts(ds):
+    """Table sets above 2^32 rows take K2's 64-bit-count form (bitmaps only:
+    2 x 560 MB)."""
+    rows = {0: 3_000_000_000, 1: 1_500_000_017}
+    tr = ds.ModelTracker(rows)
+    marks = {0: np.array([0, 5, 2_999_999_999, 1 << 31, 2_999_999_000]),
+             1: np.array([1_500_000_016, 12, 12, 0])}
+    for t, m in marks.items():
+        tr.mark(t, m)
+    view = tr.capture()
+    for t, m in marks.items():
+        assert np.array_equal(view.interval_rows[t], np.unique(m)), t
