@@ -779,16 +779,21 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
             r.i0 = r.ok ? (tile - s_sched[r.t]) * TR : 0;
             r.nrow = r.ok ? (int)min((int64_t)TR, s_sched[nt + 1 + r.t] - r.i0) : 0;
             r.loc = -1;
+            // the raw id only: nothing here may consume the load, or the warp
+            // waits for it now instead of a tile later (resolve())
+            if (lane < r.nrow)
+                r.loc = a.incremental ? a.ids[s_sched[2 * nt + 1 + r.t] + r.i0 + lane] : r.i0 + lane;
+            return r;
+        };
+        // raw id -> table-local row, validated (-2: out of range); once per tile,
+        // a tile after its load was issued
+        auto resolve = [&](TI &r) {
             if (lane < r.nrow) {
                 const ds_table_desc &td = a.t[r.t];
-                int64_t loc = r.i0 + lane;
-                if (a.incremental) {  // ids from capture are table-local; plan ids are global
-                    const int64_t raw = a.ids[s_sched[2 * nt + 1 + r.t] + r.i0 + lane];
-                    loc = a.ids_local ? raw : raw - td.row_base;
-                }
-                r.loc = (loc < 0 || loc >= td.rows) ? -2 : loc;  // -2: out of range
+                // ids from capture are table-local; plan ids are global
+                const int64_t loc = (a.incremental && !a.ids_local) ? r.loc - td.row_base : r.loc;
+                r.loc = (loc < 0 || loc >= td.rows) ? -2 : loc;
             }
-            return r;
         };
         // chunk `sub` of tile T into ring stage st (one row per lane group)
         auto issue = [&](const TI &T, int sub, int st) {
@@ -817,6 +822,8 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
             cp_async_commit();
         };
         TI cur = tinfo(0), nxt = tinfo(1);
+        resolve(cur);
+        resolve(nxt);
         // prologue: the first NS-1 chunks of the warp's chunk stream
         int isub = 0, irel = 0, ist = 0;  // next chunk to issue: sub-chunk, tile (0 cur, 1 nxt), stage
 #pragma unroll
@@ -890,6 +897,7 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
             __syncwarp();  // the stage is rewritten by the next tile
             cur = nxt;
             nxt = far;
+            resolve(nxt);
         }
         cp_async_wait<0>();  // nothing may land after the warp exits
         if (MODE == 1 && !FIXIN) {
