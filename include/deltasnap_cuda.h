@@ -62,6 +62,8 @@ typedef enum {
 #define DS_FLAG_DATA 0x2u      /* NaN/Inf element in a coded row   -> DataError      */
 #define DS_FLAG_FORMAT 0x4u    /* nonzero padding bits / bad code  -> FormatError    */
 #define DS_FLAG_INTEGRITY 0x8u /* restore row id out of range      -> IntegrityError */
+#define DS_FLAG_CAPACITY 0x10u /* output / staging buffer too small -> ValueError    */
+#define DS_FLAG_TIMEOUT 0x20u  /* peer count exchange: a rank never published     */
 
 /* Library identity / diagnostics. */
 DS_API const char *ds_version(void);
@@ -295,6 +297,42 @@ DS_API int ds_train_apply_sorted(const ds_train_table *tables_host, int ntables,
 DS_API size_t ds_crc32_workspace_size(int64_t n);
 DS_API int ds_crc32(const uint8_t *data, int64_t n, uint32_t *out, void *workspace,
                     size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Row-sharded count exchange over NVLink peer memory     */
+/* ------------------------------------------------------------------ */
+
+/* The one exchange of the row-sharded checkpoint: every rank's int64[n]
+ * dirty counts (ds_capture's per-table counts + total) to every rank, so
+ * each knows where its records land in the shard payload.  Instead of a
+ * collective running beside the writer (a NCCL kernel holds SMs the writer's
+ * resident CTAs need), the capture stream stores the counts straight into
+ * every peer's exchange buffer over NVLink (CUDA IPC), and a one-warp wait
+ * after the writer finds them already there.
+ *
+ * Exchange buffer (ds_peer_buffer_size(world, n) bytes, own cudaMalloc,
+ * zero-filled): flags uint32[2][world] (epoch of the slot), then int64
+ * slots[2][world][n]; epoch e uses parity e & 1.
+ *   ds_peer_alloc   cudaMalloc + zero + cudaIpcGetMemHandle (64-byte handle out)
+ *   ds_peer_open    cudaIpcOpenMemHandle of a peer's handle (lazy peer access)
+ *   ds_peer_close / ds_peer_free
+ *   ds_counts_publish  counts -> slot[e & 1][rank] of every peer, then
+ *                      (system-scope release) flag[e & 1][rank] = e
+ *   ds_counts_wait     until every flag[e & 1][*] == e (acquire; a rank
+ *                      missing after timeout_ns sets DS_FLAG_TIMEOUT and
+ *                      stops waiting), then slots[e & 1] -> out[world * n]
+ * epoch must grow by one per exchange, starting at 1; a rank may publish
+ * epoch e + 1 only after its own wait for e (program order on one stream
+ * gives that), so a slot is never overwritten before every rank read it. */
+DS_API size_t ds_peer_buffer_size(int world, int n);
+DS_API int ds_peer_alloc(size_t bytes, void **ptr, uint8_t *handle64);
+DS_API int ds_peer_open(const uint8_t *handle64, void **ptr);
+DS_API int ds_peer_close(void *ptr);
+DS_API int ds_peer_free(void *ptr);
+DS_API int ds_counts_publish(const int64_t *counts, int n, void *const *peers_host, int world,
+                             int rank, uint32_t epoch, void *stream);
+DS_API int ds_counts_wait(const void *local, int n, int world, uint32_t epoch, int64_t *out,
+                          uint32_t *flags, int64_t timeout_ns, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* Row-matrix codec entry points (quant.py API mirror)                  */

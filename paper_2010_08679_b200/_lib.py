@@ -33,6 +33,7 @@ FLAG_DATA = 0x2
 FLAG_FORMAT = 0x4
 FLAG_INTEGRITY = 0x8
 FLAG_CAPACITY = 0x10
+FLAG_TIMEOUT = 0x20
 
 STAT_EXACT_DECISIONS = 0
 STAT_EXACT_CODES = 1
@@ -124,6 +125,13 @@ _SIGNATURES = {
     "ds_train_apply_sorted": (_I, [_P, _I, _P, _I64, _P, _P, _P, _P, _P]),
     "ds_crc32_workspace_size": (_SZ, [_I64]),
     "ds_crc32": (_I, [_P, _I64, _P, _P, _SZ, _P]),
+    "ds_peer_buffer_size": (_SZ, [_I, _I]),
+    "ds_peer_alloc": (_I, [_SZ, _P, _P]),
+    "ds_peer_open": (_I, [_P, _P]),
+    "ds_peer_close": (_I, [_P]),
+    "ds_peer_free": (_I, [_P]),
+    "ds_counts_publish": (_I, [_P, _I, _P, _I, _I, ctypes.c_uint32, _P]),
+    "ds_counts_wait": (_I, [_P, _I, _I, ctypes.c_uint32, _P, _P, _I64, _P]),
     "ds_quantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),
     "ds_dequantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P, _P]),
     "ds_reconstruction_errors": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),
@@ -190,6 +198,8 @@ def raise_flags(flags: int, what: str) -> None:
     """
     if not flags:
         return
+    if flags & FLAG_TIMEOUT:
+        raise RuntimeError(f"{what}: a rank never published its counts (peer exchange timed out)")
     if flags & FLAG_CAPACITY:
         raise ValueError(f"{what}: output buffer too small")
     if flags & FLAG_FORMAT:

@@ -18,8 +18,6 @@
 #include "ds_common.cuh"
 #include "ds_host.h"
 
-#define DS_FLAG_CAPACITY 0x10u
-
 namespace ds {
 
 constexpr int WT = 256;  // threads per writer CTA

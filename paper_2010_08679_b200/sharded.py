@@ -8,14 +8,20 @@ counts (NCCL over NVLink, a few hundred bytes): it fixes where each rank's
 records land inside the shard payload, because a CNR1 section is one header
 followed by fixed-size records in ascending row order (payload.py:84-104), so
 the concatenation of the ranks' runs in rank order IS the reference section.
+On GPUs the counts go over NVLink peer memory (PeerCounts: stored by the
+capture stream into every peer's buffer, read after the writer); the NCCL
+all_gather (gather_counts) remains for gloo groups and DS_COUNTS_EXCHANGE=nccl.
 
 ShardedCheckpointer.step() is the stall-window work of one checkpoint
 interval (engine.py:272-281 + the writer of :339-345): K1 over the
-interval's lookups, K2 capture + fold, the count all_gather, K3.  Nothing
+interval's lookups, K2 capture + fold, the count exchange, K3.  Nothing
 synchronises the host until fetch().
 """
 
 from __future__ import annotations
+
+import ctypes
+import os
 
 import numpy as np
 import torch
@@ -24,6 +30,84 @@ from . import _lib
 from .engine import DeviceTable, ShardWriter, adaptive_for
 from .payload import HEADER_SIZE, pack_header
 from .tracker import LookupStream, ModelTracker
+
+
+class PeerCounts:
+    """The count exchange over NVLink peer memory (ds_counts_publish/_wait).
+
+    Every rank owns one exchange buffer (ds_peer_alloc); the IPC handles are
+    swapped once at construction (all_gather_object) and every peer's buffer
+    is mapped here.  publish() stores this rank's counts into every peer's
+    slot from the calling stream; finish() waits (one warp, bounded by
+    timeout_ns) until every rank's slot of the epoch is there and copies them
+    to `out`.  include/deltasnap_cuda.h gives the protocol.
+    """
+
+    def __init__(self, n: int, world: int, rank: int, group=None, device=None,
+                 timeout_s: float = 60.0):
+        import torch.distributed as dist
+        L = _lib.lib()
+        self.n, self.world, self.rank = n, world, rank
+        self.device = device
+        self.timeout_ns = int(timeout_s * 1e9)
+        size = L.ds_peer_buffer_size(world, n)
+        own = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        with torch.cuda.device(device):
+            _lib.check(L.ds_peer_alloc(size, ctypes.byref(own), handle), "peer_alloc")
+            self._own = own.value
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            ptrs, self._opened = [], []
+            for r, h in enumerate(handles):
+                if r == rank:
+                    ptrs.append(self._own)
+                    continue
+                p = ctypes.c_void_p()
+                hb = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+                _lib.check(L.ds_peer_open(hb, ctypes.byref(p)), "peer_open")
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+        self._peers = (ctypes.c_void_p * world)(*ptrs)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+        self.epoch = 0
+
+    def publish(self, counts: torch.Tensor) -> None:
+        self.epoch += 1
+        _lib.check(_lib.lib().ds_counts_publish(
+            counts.data_ptr(), self.n, ctypes.cast(self._peers, ctypes.c_void_p), self.world,
+            self.rank, self.epoch, _lib.stream_handle()), "counts_publish")
+
+    def finish(self, out: torch.Tensor) -> None:
+        _lib.check(_lib.lib().ds_counts_wait(
+            self._own, self.n, self.world, self.epoch, out.data_ptr(), self.flags.data_ptr(),
+            self.timeout_ns, _lib.stream_handle()), "counts_wait")
+
+    def check(self) -> None:
+        _lib.raise_flags(int(self.flags.item()), "count exchange")
+
+    def close(self) -> None:
+        """Unmap the peers' buffers and free this rank's (every rank must be
+        done with the exchange: callers barrier first)."""
+        L = _lib.lib()
+        with torch.cuda.device(self.device):
+            for p in self._opened:
+                L.ds_peer_close(p)
+            self._opened = []
+            if self._own:
+                L.ds_peer_free(self._own)
+                self._own = None
+
+
+def _use_peer_exchange(device, world: int, group) -> bool:
+    """The peer exchange needs CUDA tables, an NCCL group (one box) and
+    DS_COUNTS_EXCHANGE != "nccl" (the collective, kept for A/B)."""
+    if world <= 1 or device.type != "cuda":
+        return False
+    if os.environ.get("DS_COUNTS_EXCHANGE", "peer") == "nccl":
+        return False
+    import torch.distributed as dist
+    return dist.is_initialized() and dist.get_backend(group) == "nccl"
 
 
 class ShardedCheckpointer:
@@ -57,7 +141,10 @@ class ShardedCheckpointer:
         self.capacity = sum(hdr + t.rows * self.rec for t in tables)
         self.payload = torch.empty(self.capacity + 16, dtype=torch.uint8, device=self.device)
         self._seg_cache = None
-        self._comm = torch.cuda.Stream(self.device) if world_size > 1 else None
+        self._peer = PeerCounts(self.nt + 1, world_size, rank, group, self.device) \
+            if _use_peer_exchange(self.device, world_size, group) else None
+        self._comm = torch.cuda.Stream(self.device) \
+            if (world_size > 1 and self._peer is None) else None
         self._stage_buf = None
         self._side = None
         self._pending = None
@@ -85,19 +172,37 @@ class ShardedCheckpointer:
         tables once the current stream passes it.  fetch()/layout() wait for
         the side stream.  (A dirty count above staged_rows raises at fetch.)
         """
+        self.wait()  # a staged writer still reading ids / counts of the last one
         fold = 1
         self.counts = self.tracker.capture_into(self.ids, None, fold=fold, scope=self.scope)
         if staged_rows > 0:
             return self._checkpoint_staged(staged_rows)
-        if self.world > 1:
-            main = torch.cuda.current_stream(self.device)
-            self._comm.wait_stream(main)
-            with torch.cuda.stream(self._comm):
-                gather_counts(self.counts, self.world, self.group, out=self.all_counts)
-            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
-            main.wait_stream(self._comm)
-        else:
-            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
+        self.exchange_begin()
+        self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
+        self.exchange_end()
+
+    def exchange_begin(self) -> None:
+        """Start the count exchange (after K2, on the current stream): peer
+        stores of this rank's counts (PeerCounts), or the NCCL all_gather on a
+        side stream.  Nothing to do on one rank."""
+        if self.world == 1:
+            return
+        if self._peer is not None:
+            self._peer.publish(self.counts)
+            return
+        main = torch.cuda.current_stream(self.device)
+        self._comm.wait_stream(main)
+        with torch.cuda.stream(self._comm):
+            gather_counts(self.counts, self.world, self.group, out=self.all_counts)
+
+    def exchange_end(self) -> None:
+        """Every rank's counts in all_counts once the current stream passes here."""
+        if self.world == 1:
+            return
+        if self._peer is not None:
+            self._peer.finish(self.all_counts)
+            return
+        torch.cuda.current_stream(self.device).wait_stream(self._comm)
 
     def _checkpoint_staged(self, cap: int):
         main = torch.cuda.current_stream(self.device)
@@ -110,8 +215,8 @@ class ShardedCheckpointer:
         stall_end.record(main)
         self._side.wait_event(stall_end)
         with torch.cuda.stream(self._side):
-            if self.world > 1:
-                gather_counts(self.counts, self.world, self.group, out=self.all_counts)
+            self.exchange_begin()
+            self.exchange_end()
             self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True,
                               staged=self._stage_buf[:cap])
         self._pending = self._side
@@ -133,6 +238,8 @@ class ShardedCheckpointer:
         """(local payload bytes, per-table local counts, per-table totals,
         section offsets, this rank's run offsets) after a sync; see shard_layout."""
         self.wait()
+        if self._peer is not None:
+            self._peer.check()
         counts_all = self.all_counts.view(self.world, self.nt + 1).cpu().numpy() \
             if self.world > 1 else self.counts.view(1, self.nt + 1).cpu().numpy()
         per_table, sec_off, run_off = shard_layout(counts_all[:, :self.nt], self.rank, self.rec)

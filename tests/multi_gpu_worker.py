@@ -1,9 +1,10 @@
 """Rank program of tests/test_multi_gpu.py (torchrun, NCCL, one GPU per rank).
 
 Each rank holds contiguous row shards of every table, marks its share of a
-global Zipf-like lookup stream, runs K2 + the NCCL count all_gather + K3
-(ShardedCheckpointer.step), and rank 0 assembles the shard payload from every
-rank's D2H'd runs.  It must equal the oracle's single-process payload of the
+global Zipf-like lookup stream, runs K2 + the count exchange (NVLink peer
+stores, or the NCCL all_gather with DS_COUNTS_EXCHANGE=nccl) + K3
+(ShardedCheckpointer.step; the second of three intervals staged), and rank 0
+assembles the shard payload from every rank's D2H'd runs.  It must equal the oracle's single-process payload of the
 whole tables (engine.py:118-189) byte for byte.
 """
 import os
@@ -32,7 +33,6 @@ def main():
     dist.init_process_group("nccl", device_id=dev)
     rng = np.random.default_rng(42)
     full = {t: rng.standard_normal((r, dim)).astype(np.float32) for t, r in ROWS.items()}
-    look = {t: np.minimum(rng.zipf(1.2, 50_000) - 1, r - 1).astype(np.int64) for t, r in ROWS.items()}
     shapes = {t: (r, dim) for t, r in ROWS.items()}
 
     def init(tid, lo, v):
@@ -40,33 +40,48 @@ def main():
 
     tables = make_local_tables(shapes, world, rank, dev, init)
     ck = ShardedCheckpointer(tables, bitwidth, rank=rank, world_size=world, device=dev)
-    idx, seg = [], [0]
-    for t in sorted(ROWS):
-        lo, hi = shard_rows(ROWS[t], world, rank)
-        mine = look[t][(look[t] >= lo) & (look[t] < hi)] - lo
-        idx.append(mine)
-        seg.append(seg[-1] + mine.size)
-    sel = {}  # this rank's dirty rows, global ids
-    for k, t in enumerate(sorted(ROWS)):
-        lo, hi = shard_rows(ROWS[t], world, rank)
-        sel[t] = np.unique(idx[k]) + lo
-    ids = torch.from_numpy(np.concatenate(idx)).to(torch.int32).to(dev)
-    ck.step(ids, np.array(seg), np.arange(len(ROWS)))
-    torch.cuda.synchronize()
-    buf, n = ck.fetch()
-    torch.cuda.synchronize()
-    _, local_counts, per_table, _, _ = ck.layout()
-    mine = (bytes(buf[:n].numpy()), np.asarray(local_counts).copy())
-    got = [None] * world
-    dist.all_gather_object(got, mine)
-    sels = [None] * world
-    dist.all_gather_object(sels, sel)
-    if rank == 0:
-        blob = ck.assemble(got, per_table)
-        gsel = {t: np.sort(np.concatenate([s[t] for s in sels])) for t in ROWS}
-        ref, _, _ = O.build_shard_payload({t: (full[t], None) for t in ROWS}, "incremental", gsel,
-                                          bitwidth, sorted(ROWS))
-        print("OK" if blob == ref else f"MISMATCH {len(blob)} {len(ref)}", flush=True)
+    want_peer = os.environ.get("DS_COUNTS_EXCHANGE", "peer") != "nccl"
+    assert (ck._peer is not None) == want_peer, "count exchange transport"
+    # three intervals (exchange epochs 1..3, both slot parities); the second
+    # one through stall-window staging
+    ok = True
+    for interval in range(3):
+        look = {t: np.minimum(rng.zipf(1.2, 50_000) - 1, r - 1).astype(np.int64) for t, r in ROWS.items()}
+        idx, seg = [], [0]
+        for t in sorted(ROWS):
+            lo, hi = shard_rows(ROWS[t], world, rank)
+            mine = look[t][(look[t] >= lo) & (look[t] < hi)] - lo
+            idx.append(mine)
+            seg.append(seg[-1] + mine.size)
+        sel = {}  # this rank's dirty rows, global ids
+        for k, t in enumerate(sorted(ROWS)):
+            lo, hi = shard_rows(ROWS[t], world, rank)
+            sel[t] = np.unique(idx[k]) + lo
+        ids = torch.from_numpy(np.concatenate(idx)).to(torch.int32).to(dev)
+        if interval == 1:
+            ck.mark(ids, np.array(seg), np.arange(len(ROWS)))
+            ck.checkpoint(staged_rows=sum(ROWS.values()))
+        else:
+            ck.step(ids, np.array(seg), np.arange(len(ROWS)))
+        torch.cuda.synchronize()
+        buf, n = ck.fetch()
+        torch.cuda.synchronize()
+        _, local_counts, per_table, _, _ = ck.layout()
+        mine = (bytes(buf[:n].numpy()), np.asarray(local_counts).copy())
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        sels = [None] * world
+        dist.all_gather_object(sels, sel)
+        if rank == 0:
+            blob = ck.assemble(got, per_table)
+            gsel = {t: np.sort(np.concatenate([s[t] for s in sels])) for t in ROWS}
+            ref, _, _ = O.build_shard_payload({t: (full[t], None) for t in ROWS}, "incremental", gsel,
+                                              bitwidth, sorted(ROWS))
+            if blob != ref:
+                ok = False
+                print(f"MISMATCH interval {interval}: {len(blob)} {len(ref)}", flush=True)
+    if rank == 0 and ok:
+        print("OK", flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
