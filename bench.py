@@ -411,9 +411,7 @@ def run_ours(args):
             ev[k][1].record()
             ck.counts = ck.tracker.capture_into(ck.ids, None, fold=1, scope=ck.scope)  # K2
             ev[k][2].record()
-            ck.exchange_begin()  # N > 1: counts to every peer (NVLink stores), beside K3
-            ck.writer.write(ck.payload, ck.ids, ck.counts[:ck.nt], None, local_ids=True)  # K3
-            ck.exchange_end()    # every rank's counts (already there: a one-warp read)
+            ck.write()  # K3 (N > 1: + the count exchange over NVLink peer memory, same launch)
             ev[k][3].record()
         torch.cuda.synchronize()
     barrier()

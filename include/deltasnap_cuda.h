@@ -178,6 +178,9 @@ typedef struct {
     const float *staged;       /* optional: rows already gathered by ds_stage_rows (record i
                                   of the packed id order at staged[i * dim]); the tables are
                                   then only used for bounds, row_base and dims */
+    const struct ds_peer_exchange *exchange; /* NULL, or the row-sharded count exchange run
+                                  inside this launch (below): CTA 0 publishes, the last
+                                  CTA waits for every rank and writes exchange->out */
 } ds_ckpt_params;
 
 /* Counters of the certified fast path (diagnostics). */
@@ -302,37 +305,42 @@ DS_API int ds_crc32(const uint8_t *data, int64_t n, uint32_t *out, void *workspa
 /* Row-sharded count exchange over NVLink peer memory     */
 /* ------------------------------------------------------------------ */
 
-/* The one exchange of the row-sharded checkpoint: every rank's int64[n]
- * dirty counts (ds_capture's per-table counts + total) to every rank, so
- * each knows where its records land in the shard payload.  Instead of a
- * collective running beside the writer (a NCCL kernel holds SMs the writer's
- * resident CTAs need), the capture stream stores the counts straight into
- * every peer's exchange buffer over NVLink (CUDA IPC), and a one-warp wait
- * after the writer finds them already there.
+/* The one exchange of the row-sharded checkpoint: every rank's int64
+ * dirty counts (per table, then their total) to every rank, so each knows
+ * where its records land in the shard payload.  A collective beside the
+ * writer costs more than its bytes (its kernel holds SMs that the writer's
+ * resident CTAs need), so the exchange runs inside the writer's launch
+ * (ds_ckpt_params.exchange): CTA 0 stores this rank's counts into every
+ * peer's exchange buffer over NVLink (CUDA IPC mappings) and releases the
+ * slot's epoch flag at system scope; the last CTA to finish waits (acquire)
+ * until every rank's flag shows the epoch -- normally already true, the
+ * peers published when their writers started -- and copies the slots out.
  *
- * Exchange buffer (ds_peer_buffer_size(world, n) bytes, own cudaMalloc,
- * zero-filled): flags uint32[2][world] (epoch of the slot), then int64
- * slots[2][world][n]; epoch e uses parity e & 1.
+ * Exchange buffer (ds_peer_buffer_size(world, ntables + 1) bytes, own
+ * cudaMalloc, zero-filled): flags uint32[2][world], then int64
+ * slots[2][world][ntables + 1]; epoch e uses parity e & 1.  The epoch must
+ * grow by one per exchange starting at 1, and every rank runs the same
+ * sequence of exchanges; a rank publishes e + 1 only after its own wait for
+ * e (stream order gives that), so no slot is overwritten before every rank
+ * has read it.  A rank missing after timeout_ns sets DS_FLAG_TIMEOUT in
+ * *flags and the wait gives up.
  *   ds_peer_alloc   cudaMalloc + zero + cudaIpcGetMemHandle (64-byte handle out)
  *   ds_peer_open    cudaIpcOpenMemHandle of a peer's handle (lazy peer access)
- *   ds_peer_close / ds_peer_free
- *   ds_counts_publish  counts -> slot[e & 1][rank] of every peer, then
- *                      (system-scope release) flag[e & 1][rank] = e
- *   ds_counts_wait     until every flag[e & 1][*] == e (acquire; a rank
- *                      missing after timeout_ns sets DS_FLAG_TIMEOUT and
- *                      stops waiting), then slots[e & 1] -> out[world * n]
- * epoch must grow by one per exchange, starting at 1; a rank may publish
- * epoch e + 1 only after its own wait for e (program order on one stream
- * gives that), so a slot is never overwritten before every rank read it. */
+ *   ds_peer_close / ds_peer_free */
+#define DS_PEER_MAX 64
+typedef struct ds_peer_exchange {
+    void *peers[DS_PEER_MAX]; /* every rank's exchange buffer, this rank's included */
+    int64_t *out;             /* device int64[world * (ntables + 1)], rank-major */
+    uint32_t *flags;          /* device flag word for DS_FLAG_TIMEOUT */
+    int64_t timeout_ns;
+    int world, rank;
+    uint32_t epoch;
+} ds_peer_exchange;
 DS_API size_t ds_peer_buffer_size(int world, int n);
 DS_API int ds_peer_alloc(size_t bytes, void **ptr, uint8_t *handle64);
 DS_API int ds_peer_open(const uint8_t *handle64, void **ptr);
 DS_API int ds_peer_close(void *ptr);
 DS_API int ds_peer_free(void *ptr);
-DS_API int ds_counts_publish(const int64_t *counts, int n, void *const *peers_host, int world,
-                             int rank, uint32_t epoch, void *stream);
-DS_API int ds_counts_wait(const void *local, int n, int world, uint32_t epoch, int64_t *out,
-                          uint32_t *flags, int64_t timeout_ns, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* Row-matrix codec entry points (quant.py API mirror)                  */

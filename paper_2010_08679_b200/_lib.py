@@ -68,6 +68,23 @@ class CkptParams(ctypes.Structure):
         ("ids_local", ctypes.c_int),
         ("stats", ctypes.c_void_p),
         ("staged", ctypes.c_void_p),
+        ("exchange", ctypes.c_void_p),
+    ]
+
+
+PEER_MAX = 64
+
+
+class PeerExchange(ctypes.Structure):
+    """ds_peer_exchange: the row-sharded count exchange run inside K3."""
+    _fields_ = [
+        ("peers", ctypes.c_void_p * PEER_MAX),
+        ("out", ctypes.c_void_p),
+        ("flags", ctypes.c_void_p),
+        ("timeout_ns", ctypes.c_int64),
+        ("world", ctypes.c_int),
+        ("rank", ctypes.c_int),
+        ("epoch", ctypes.c_uint32),
     ]
 
 
@@ -130,8 +147,6 @@ _SIGNATURES = {
     "ds_peer_open": (_I, [_P, _P]),
     "ds_peer_close": (_I, [_P]),
     "ds_peer_free": (_I, [_P]),
-    "ds_counts_publish": (_I, [_P, _I, _P, _I, _I, ctypes.c_uint32, _P]),
-    "ds_counts_wait": (_I, [_P, _I, _I, ctypes.c_uint32, _P, _P, _I64, _P]),
     "ds_quantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),
     "ds_dequantize_rows": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P, _P]),
     "ds_reconstruction_errors": (_I, [_P, _I64, _I64, _P, _P, _I, _P, _P]),

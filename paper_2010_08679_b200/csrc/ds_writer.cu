@@ -223,6 +223,17 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         return host::fail(DS_ERR_ARG, "ds_write_payload: staged rows need an incremental "
                                       "checkpoint with packed ids and no aux");
 
+    a.has_x = p->exchange != nullptr;
+    if (a.has_x) {
+        const ds_peer_exchange &x = *p->exchange;
+        if (x.world < 1 || x.world > DS_PEER_MAX || x.rank < 0 || x.rank >= x.world || x.epoch == 0 ||
+            !x.out || !x.flags)
+            return host::fail(DS_ERR_ARG, "ds_write_payload: bad count exchange");
+        for (int r = 0; r < x.world; r++)
+            if (!x.peers[r]) return host::fail(DS_ERR_ARG, "ds_write_payload: null peer buffer");
+        a.x = x;
+    }
+
     const int mode = bw == 0 ? 0 : (p->adaptive_bins > 0 ? 2 : 1);
     Cfg c = pick_cfg(d, vec4, mode);
     const bool pad = (c.VEC == 4 ? 4 * c.G * c.C : c.G * c.C) != d;

@@ -53,7 +53,77 @@ struct WriterArgs {
     uint32_t *flags;
     unsigned long long *stats;
     const float *staged;  // rows gathered by ds_stage_rows (read record i of the packed order)
+    int has_x;            // the row-sharded count exchange runs in this launch
+    ds_peer_exchange x;
 };
+
+// ---------------------------------------------------------------------------
+// the row-sharded count exchange (include/deltasnap_cuda.h, ds_peer.cu)
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t peer_flags_bytes(int world) {
+    return ((size_t)2 * world * sizeof(uint32_t) + 255) & ~(size_t)255;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// one warp: this rank's counts (per table from the layout, then the total)
+// into slot [e & 1][rank] of every peer's buffer, then the slot's flag
+__device__ __forceinline__ void peer_publish(const WriterArgs &a, const int64_t *s_sched) {
+    const int lane = threadIdx.x & 31, nt = a.ntables, n = nt + 1;
+    const ds_peer_exchange &x = a.x;
+    const int par = x.epoch & 1;
+    int64_t tot = 0;
+    for (int t = lane; t < nt; t += 32) tot += s_sched[nt + 1 + t];
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(DS_FULL_MASK, tot, o);
+    for (int p = 0; p < x.world; p++) {
+        uint8_t *base = static_cast<uint8_t *>(x.peers[p]);
+        int64_t *slot = reinterpret_cast<int64_t *>(base + peer_flags_bytes(x.world)) +
+                        ((size_t)par * x.world + x.rank) * n;
+        for (int t = lane; t < n; t += 32) slot[t] = t < nt ? s_sched[nt + 1 + t] : tot;
+    }
+    __syncwarp();
+    __threadfence_system();  // every slot before any flag, for every observer
+    if (lane < x.world)
+        st_release_sys(reinterpret_cast<uint32_t *>(x.peers[lane]) + par * x.world + x.rank, x.epoch);
+}
+
+// one warp (the last CTA): until every rank's flag of the epoch is up, then
+// the slots -> x.out; DS_FLAG_TIMEOUT if a rank stays missing
+__device__ __forceinline__ void peer_wait(const WriterArgs &a) {
+    const int lane = threadIdx.x & 31, n = a.ntables + 1;
+    const ds_peer_exchange &x = a.x;
+    const int par = x.epoch & 1;
+    const uint8_t *local = static_cast<const uint8_t *>(x.peers[x.rank]);
+    const uint32_t *flags = reinterpret_cast<const uint32_t *>(local) + par * x.world;
+    bool late = false;
+    const uint64_t t0 = globaltimer_ns();
+    for (int r = lane; r < x.world; r += 32)
+        while (ld_acquire_sys(flags + r) != x.epoch) {
+            if ((int64_t)(globaltimer_ns() - t0) > x.timeout_ns) {
+                late = true;
+                break;
+            }
+            __nanosleep(64);
+        }
+    if (__any_sync(DS_FULL_MASK, late)) {
+        if (lane == 0) atomicOr(x.flags, DS_FLAG_TIMEOUT);
+        return;
+    }
+    const volatile int64_t *slots =
+        reinterpret_cast<const int64_t *>(local + peer_flags_bytes(x.world)) + (size_t)par * x.world * n;
+    for (int i = lane; i < x.world * n; i += 32) x.out[i] = slots[i];
+}
 
 // ---------------------------------------------------------------------------
 // shared-memory byte helpers
@@ -404,6 +474,9 @@ __device__ __forceinline__ void writer_layout(const WriterArgs &a, int64_t *s_sc
     __syncthreads();
     if (blockIdx.x == 0) {
         const int64_t total = s_sec[nt];
+        // the last warp publishes this rank's counts to the peers (its fence
+        // delays only that warp)
+        if (a.has_x && (threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1) peer_publish(a, s_sched);
         for (int t = threadIdx.x; t <= nt; t += blockDim.x) a.sec_off[t] = s_sec[t];
         if (threadIdx.x == 0 && total > a.capacity) atomicOr(a.flags, DS_FLAG_CAPACITY);
         if (a.write_headers && total <= a.capacity) {
@@ -465,6 +538,7 @@ __device__ __forceinline__ void writer_epilogue(const WriterArgs &a, WAcc &acc, 
             if (a.err_out) *a.err_out = s;
             *a.done = 0u;  // ready for the next call on this workspace
         }
+        if (a.has_x) peer_wait(a);
     }
 }
 

@@ -149,7 +149,7 @@ class ShardWriter:
 
     def write(self, payload: torch.Tensor, ids: torch.Tensor | None = None,
               counts: torch.Tensor | None = None, ids_offsets=None, *, local_ids: bool = False,
-              stream=None, staged: torch.Tensor | None = None) -> None:
+              stream=None, staged: torch.Tensor | None = None, exchange=None) -> None:
         """Launch layout + writer (+ error reduction).
 
         Incremental when `ids` is given: ids concatenates every table's row
@@ -158,6 +158,8 @@ class ShardWriter:
         None means "packed" -- the starts are the prefix sums of counts,
         computed on the device (capture's layout, no host sync).  local_ids:
         the ids are table-local rows (capture output) instead of global ids.
+        exchange: a ctypes ds_peer_exchange (sharded.PeerCounts.arg) -- the
+        row-sharded count exchange then runs inside this launch.
         """
         incremental = ids is not None
         self.params.incremental = int(incremental)
@@ -165,6 +167,7 @@ class ShardWriter:
         self.params.ids_local = int(local_ids)
         # rows gathered by stage_rows (packed id order) instead of the live tables
         self.params.staged = staged.data_ptr() if staged is not None else None
+        self.params.exchange = ctypes.addressof(exchange) if exchange is not None else None
         if incremental and ids_offsets is not None:
             for k in range(len(self.tables)):
                 self._descs[k].ids_off = int(ids_offsets[k])

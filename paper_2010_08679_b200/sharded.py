@@ -8,9 +8,10 @@ counts (NCCL over NVLink, a few hundred bytes): it fixes where each rank's
 records land inside the shard payload, because a CNR1 section is one header
 followed by fixed-size records in ascending row order (payload.py:84-104), so
 the concatenation of the ranks' runs in rank order IS the reference section.
-On GPUs the counts go over NVLink peer memory (PeerCounts: stored by the
-capture stream into every peer's buffer, read after the writer); the NCCL
-all_gather (gather_counts) remains for gloo groups and DS_COUNTS_EXCHANGE=nccl.
+On GPUs the counts go over NVLink peer memory inside the writer's launch
+(PeerCounts: CTA 0 stores them into every peer's buffer, the last CTA reads
+every rank's); the NCCL all_gather (gather_counts) remains for gloo groups
+and DS_COUNTS_EXCHANGE=nccl.
 
 ShardedCheckpointer.step() is the stall-window work of one checkpoint
 interval (engine.py:272-281 + the writer of :339-345): K1 over the
@@ -33,23 +34,25 @@ from .tracker import LookupStream, ModelTracker
 
 
 class PeerCounts:
-    """The count exchange over NVLink peer memory (ds_counts_publish/_wait).
+    """The count exchange over NVLink peer memory, run inside K3.
 
     Every rank owns one exchange buffer (ds_peer_alloc); the IPC handles are
     swapped once at construction (all_gather_object) and every peer's buffer
-    is mapped here.  publish() stores this rank's counts into every peer's
-    slot from the calling stream; finish() waits (one warp, bounded by
-    timeout_ns) until every rank's slot of the epoch is there and copies them
-    to `out`.  include/deltasnap_cuda.h gives the protocol.
+    is mapped here.  arg(out) is the ds_peer_exchange of the next epoch for
+    ShardWriter.write: the writer's CTA 0 stores this rank's counts into
+    every peer's slot, its last CTA waits (bounded by timeout_s) for every
+    rank's and copies them to `out`.  include/deltasnap_cuda.h gives the
+    protocol.
     """
 
     def __init__(self, n: int, world: int, rank: int, group=None, device=None,
                  timeout_s: float = 60.0):
         import torch.distributed as dist
         L = _lib.lib()
+        if world > _lib.PEER_MAX:
+            raise ValueError(f"peer count exchange: at most {_lib.PEER_MAX} ranks")
         self.n, self.world, self.rank = n, world, rank
         self.device = device
-        self.timeout_ns = int(timeout_s * 1e9)
         size = L.ds_peer_buffer_size(world, n)
         own = ctypes.c_void_p()
         handle = (ctypes.c_uint8 * 64)()
@@ -68,20 +71,23 @@ class PeerCounts:
                 _lib.check(L.ds_peer_open(hb, ctypes.byref(p)), "peer_open")
                 ptrs.append(p.value)
                 self._opened.append(p.value)
-        self._peers = (ctypes.c_void_p * world)(*ptrs)
         self.flags = torch.zeros(1, dtype=torch.int32, device=device)
-        self.epoch = 0
+        self._x = _lib.PeerExchange()
+        for r, p in enumerate(ptrs):
+            self._x.peers[r] = p
+        self._x.flags = self.flags.data_ptr()
+        self._x.timeout_ns = int(timeout_s * 1e9)
+        self._x.world, self._x.rank, self._x.epoch = world, rank, 0
 
-    def publish(self, counts: torch.Tensor) -> None:
-        self.epoch += 1
-        _lib.check(_lib.lib().ds_counts_publish(
-            counts.data_ptr(), self.n, ctypes.cast(self._peers, ctypes.c_void_p), self.world,
-            self.rank, self.epoch, _lib.stream_handle()), "counts_publish")
+    @property
+    def epoch(self) -> int:
+        return self._x.epoch
 
-    def finish(self, out: torch.Tensor) -> None:
-        _lib.check(_lib.lib().ds_counts_wait(
-            self._own, self.n, self.world, self.epoch, out.data_ptr(), self.flags.data_ptr(),
-            self.timeout_ns, _lib.stream_handle()), "counts_wait")
+    def arg(self, out: torch.Tensor):
+        """ds_peer_exchange of the next epoch, the counts landing in out."""
+        self._x.epoch += 1
+        self._x.out = out.data_ptr()
+        return self._x
 
     def check(self) -> None:
         _lib.raise_flags(int(self.flags.item()), "count exchange")
@@ -177,32 +183,27 @@ class ShardedCheckpointer:
         self.counts = self.tracker.capture_into(self.ids, None, fold=fold, scope=self.scope)
         if staged_rows > 0:
             return self._checkpoint_staged(staged_rows)
-        self.exchange_begin()
-        self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True)
-        self.exchange_end()
+        self.write()
 
-    def exchange_begin(self) -> None:
-        """Start the count exchange (after K2, on the current stream): peer
-        stores of this rank's counts (PeerCounts), or the NCCL all_gather on a
-        side stream.  Nothing to do on one rank."""
+    def write(self, staged: torch.Tensor | None = None) -> None:
+        """K3 over the captured ids, with the count exchange when N > 1: inside
+        the writer's launch over NVLink peer memory (PeerCounts), or the NCCL
+        all_gather on a side stream beside it (gloo groups,
+        DS_COUNTS_EXCHANGE=nccl).  Every rank's counts are in all_counts once
+        the current stream passes this call."""
+        args = (self.payload, self.ids, self.counts[:self.nt], None)
         if self.world == 1:
-            return
-        if self._peer is not None:
-            self._peer.publish(self.counts)
-            return
-        main = torch.cuda.current_stream(self.device)
-        self._comm.wait_stream(main)
-        with torch.cuda.stream(self._comm):
-            gather_counts(self.counts, self.world, self.group, out=self.all_counts)
-
-    def exchange_end(self) -> None:
-        """Every rank's counts in all_counts once the current stream passes here."""
-        if self.world == 1:
-            return
-        if self._peer is not None:
-            self._peer.finish(self.all_counts)
-            return
-        torch.cuda.current_stream(self.device).wait_stream(self._comm)
+            self.writer.write(*args, local_ids=True, staged=staged)
+        elif self._peer is not None:
+            self.writer.write(*args, local_ids=True, staged=staged,
+                              exchange=self._peer.arg(self.all_counts))
+        else:
+            main = torch.cuda.current_stream(self.device)
+            self._comm.wait_stream(main)
+            with torch.cuda.stream(self._comm):
+                gather_counts(self.counts, self.world, self.group, out=self.all_counts)
+            self.writer.write(*args, local_ids=True, staged=staged)
+            main.wait_stream(self._comm)
 
     def _checkpoint_staged(self, cap: int):
         main = torch.cuda.current_stream(self.device)
@@ -215,10 +216,7 @@ class ShardedCheckpointer:
         stall_end.record(main)
         self._side.wait_event(stall_end)
         with torch.cuda.stream(self._side):
-            self.exchange_begin()
-            self.exchange_end()
-            self.writer.write(self.payload, self.ids, self.counts[:self.nt], None, local_ids=True,
-                              staged=self._stage_buf[:cap])
+            self.write(staged=self._stage_buf[:cap])
         self._pending = self._side
         return stall_end
 
