@@ -125,3 +125,33 @@ def test_pack_ids_bitstream():
         assert got == a.tolist(), bits
     assert [lookup_width(r) for r in (1, 2, 3, 256, 257, 1 << 28, (1 << 28) + 1, 1 << 31,
                                       (1 << 31) + 1)] == [4, 4, 4, 8, 12, 28, 32, 32, 64]
+
+
+def test_ctypes_structs_match_the_header_layout(tmp_path):
+    """Every struct the Python binding passes through the C ABI has the
+    header's size and field offsets (gcc compiles a probe against the header)."""
+    import shutil
+    import subprocess
+    from paper_2010_08679_b200 import _lib
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    mirrors = {"ds_table_desc": _lib.TableDesc, "ds_ckpt_params": _lib.CkptParams,
+               "ds_restore_sec": _lib.RestoreSec, "ds_train_table": _lib.TrainTable,
+               "ds_peer_exchange": _lib.PeerExchange}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for c, py in mirrors.items():
+        t = c if c != "ds_peer_exchange" else "struct ds_peer_exchange"
+        lines.append(f'printf("{c} size %zu\\n", sizeof({t}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{c} {f} %zu\\n", offsetof({t}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                          check=True).stdout.splitlines())
+    for c, py in mirrors.items():
+        assert int(got[f"{c} size"]) == ctypes.sizeof(py), c
+        for f, _ in py._fields_:
+            assert int(got[f"{c} {f}"]) == getattr(py, f).offset, (c, f)
