@@ -403,9 +403,16 @@ def run_ours(args):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     barrier()
     torch.cuda.synchronize()
+    align = torch.zeros(1, dtype=torch.int32, device=dev)
     with ClockSampler(torch.cuda.current_device()) as clocks:
         for k in range(K):
             flush.fill_(k & 0xFF)
+            if world > 1:
+                # ranks leave the (untimed) flush together, as a training
+                # step's gradient collective would release them: a device-side
+                # all_reduce, no host sync.  Without it one rank's slower flush
+                # shows up as another rank's wait inside K3's count exchange.
+                dist.all_reduce(align)
             ev[k][0].record()
             ck.mark(stream)                                # K1
             ev[k][1].record()
@@ -554,7 +561,9 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": elapsed / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": dict(workload_desc(w), dirty_rows_per_step=dirty_all,
-                           parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch),
+                           parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch,
+                           **({"rank_alignment": "device all_reduce after each untimed L2 flush"}
+                              if world > 1 else {})),
             "rows_per_s": dirty_all * K / elapsed,
             "roofline": roofline, "phases": phases, "payload_crc32": crc, "staged": staged,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
