@@ -61,6 +61,12 @@ WORKLOADS = {
                             "(bins 45, ratio 0.2)",
                        cards=[125_000_000], dim=128, bitwidth=4, adaptive=True, lookups="uniform",
                        n_per_table=37_500_000),
+    # configs[3], one of 8 GPU shards of 1B x 128: the 2-bit adaptive greedy
+    # ranges (bins 25, ratio 0.5: 25 candidate evaluations per row)
+    "C4": dict(desc="C4 (one of 8 GPU shards): 125M rows x dim 128 fp32 (64 GB), 2-bit adaptive "
+                    "greedy (bins 25, ratio 0.5) incremental, 37.5M uniform lookups per interval",
+               cards=[125_000_000], dim=128, bitwidth=2, adaptive=True, lookups="uniform",
+               n_per_table=37_500_000),
     # configs[4]: restore of a full checkpoint + 5 incremental deltas
     "C5": dict(desc="C5: restore a chain (1 full + 5 incremental 8-bit checkpoints of the C2 "
                     "tables) into device tables: unpack, dequantize, scatter, baseline bits",

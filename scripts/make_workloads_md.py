@@ -3,7 +3,7 @@ import json, os, sys
 
 tag = sys.argv[1]
 rows, raw = [], []
-for wl in ["C2", "T", "T-adaptive", "C3", "C5"]:
+for wl in ["C2", "T", "T-adaptive", "C3", "C4", "C5"]:
     p = f"gpurun_out/w_{wl}.json"
     if not os.path.exists(p):
         continue
