@@ -117,7 +117,11 @@ def _use_peer_exchange(device, world: int, group) -> bool:
 
 
 class ShardedCheckpointer:
-    """One rank's part of a row-sharded incremental checkpoint."""
+    """One rank's part of a row-sharded incremental checkpoint.
+
+    With world_size > 1 on an NCCL group the constructor is collective (the
+    ranks swap their count-exchange buffers, PeerCounts), and every rank must
+    then run the same sequence of checkpoints."""
 
     def __init__(self, tables: list, bitwidth: int | None, *, adaptive_overrides: dict | None = None,
                  rank: int = 0, world_size: int = 1, group=None, device=None,
