@@ -27,6 +27,14 @@
 
 namespace ds {
 
+// Programmatic dependent launch (K1 -> K2 count -> K2 emit -> K3 on one
+// stream): a kernel lets its successor launch as soon as its own CTAs are all
+// resident, the successor's CTAs take the SMs its tail frees, and wait here
+// until it has completed and its writes are visible.  Both are no-ops for a
+// launch without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr float kU = 5.9604644775390625e-08f;  // 2^-24, unit roundoff of fp32
 
 // ---------------------------------------------------------------------------

@@ -44,6 +44,29 @@ inline int64_t env_int(const char *name, int64_t dflt) {
     return v && v[0] ? strtoll(v, nullptr, 10) : dflt;
 }
 
+// Launch with programmatic stream serialization (see ds_common.cuh pdl_*);
+// DS_PDL=0 launches normally (A/B).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t s, Args... args) {
+    static const bool on = env_int("DS_PDL", 1) != 0;
+    if (!on) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Grid for a grid-stride kernel: enough blocks to cover n, capped at
 // `per_sm` resident blocks per SM.
 inline int64_t grid_for(int64_t n, int threads, int per_sm) {

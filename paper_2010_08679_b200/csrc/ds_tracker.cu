@@ -484,6 +484,7 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
 // its row count needs, which is what bounds the end-to-end H2D of the lookup
 // stream.
 __global__ void __launch_bounds__(MARK_THREADS) mark_tma_kernel(const MarkArgs a) {
+    pdl_trigger();  // K2 may launch once every K1 CTA is resident
     extern __shared__ __align__(128) uint8_t mk_smem[];
     __shared__ __align__(8) unsigned long long bars[MK_WARPS][MK_WSTAGES];
     // dynamic shared memory: [per-warp TMA rings][cache | bit window | byte map]
@@ -820,6 +821,8 @@ __device__ __forceinline__ unsigned long long cap3_block_sum(unsigned long long 
 
 // pass 1: per-chunk popcounts, and their 256-chunk group sums
 __global__ void __launch_bounds__(CF_THREADS) cap3_count_kernel(const Cap3Args a) {
+    pdl_trigger();
+    pdl_wait();  // K1's bits
     __shared__ unsigned long long s_red[CF_THREADS / 32];
     const int c = blockIdx.x, t = cap3_table(a, c);
     uint32_t iv[C3_WPT], uv[C3_WPT];
@@ -845,6 +848,8 @@ static_assert(CAP3_STAGE * 4 <= 48 * 1024, "stage must fit static shared memory"
 // yields the thread's scan offset, the chunk's base and (last chunks) the
 // table's start together, and one before the staged ids leave.
 __global__ void __launch_bounds__(CF_THREADS) cap3_emit_kernel(const Cap3Args a) {
+    pdl_trigger();
+    pdl_wait();  // the count pass's chunk and group sums
     constexpr int NWP = CF_THREADS / 32;
     __shared__ unsigned long long s_cnt[NWP], s_base[NWP], s_start[NWP];
     __shared__ uint32_t s_ids[CAP3_STAGE];
@@ -1235,8 +1240,9 @@ extern "C" int ds_capture(uint32_t *interval, uint32_t *baseline, const int64_t 
         f.ticket = reinterpret_cast<unsigned *>(workspace);
         f.cnt = reinterpret_cast<unsigned long long *>(static_cast<uint8_t *>(workspace) + 16);
         f.super = f.cnt + nch;
-        cap3_count_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
-        cap3_emit_kernel<<<(unsigned)nch, CF_THREADS, 0, s>>>(f);
+        cudaError_t e = host::launch_pdl(cap3_count_kernel, (unsigned)nch, CF_THREADS, 0, s, f);
+        if (e == cudaSuccess) e = host::launch_pdl(cap3_emit_kernel, (unsigned)nch, CF_THREADS, 0, s, f);
+        if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
         return host::check_launch("ds_capture");
     }
     CapArgs a;

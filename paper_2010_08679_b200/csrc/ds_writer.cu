@@ -281,7 +281,8 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     if (grid > 4096) grid = 4096;
 
     // one launch: layout, records, exact fixups and the error sum
-    fn<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(a);
+    e = host::launch_pdl(fn, (unsigned)grid, (unsigned)threads, smem, (cudaStream_t)stream, a);
+    if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     return host::check_launch("ds_write_payload");
 }
 

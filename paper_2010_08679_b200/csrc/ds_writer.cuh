@@ -783,6 +783,7 @@ __host__ __device__ constexpr int writer_stages() { return G == 1 ? DS_WRITER_NS
 template <int G, int C, int VEC, int MODE, bool PAD>
 __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
     writer_warp_kernel(const WriterArgs a) {
+    pdl_wait();  // K2's ids and counts (PDL launch after the emit pass)
     constexpr int EPL = C * VEC;
     constexpr int RPC = 32 / G;  // rows per chunk
     constexpr int NS = writer_stages<G>();
@@ -996,6 +997,7 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
 // ---------------------------------------------------------------------------
 template <int G, int C, int VEC, int MODE, bool PAD>
 __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
+    pdl_wait();
     constexpr int EPL = C * VEC;
     constexpr int RPP = WT / G;  // rows per pass
     extern __shared__ __align__(16) uint8_t smem[];
