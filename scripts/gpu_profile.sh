@@ -13,7 +13,7 @@ CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu"
 timeout 300 $CMD > $OUT/plain.log 2>&1; rc=$?; echo "plain rc=$rc"
 if [ $rc -eq 0 ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
-      -k regex:"mark_tma|cap3|writer_warp|writer_kernel|restore_kernel" -c 42 --csv \
+      -k regex:"mark_tma|cap3|writer_warp|writer_kernel|restore" -c 42 --csv \
       --log-file $OUT/launches.csv $CMD > $OUT/ncu_launches.log 2>&1; echo "ncu launches rc=$?"
   timeout 900 ncu --set full --clock-control none --import-source on \
       -k regex:"${NCU_K:-writer_warp|mark_tma|cap3_count|cap3_emit}" -s ${NCU_S:-16} -c ${NCU_C:-4} \
