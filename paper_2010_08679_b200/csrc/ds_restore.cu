@@ -153,6 +153,10 @@ __device__ __forceinline__ uint32_t lds32u(const uint8_t *base, int o) {
 template <int G>
 __global__ void __launch_bounds__(RT) restore_payload_kernel(const RestorePArgs a) {
     extern __shared__ __align__(16) uint8_t stage[];
+    // chained payloads (PDL): the next one launches into this one's tail and
+    // waits here until it is complete (later payloads override earlier rows)
+    pdl_trigger();
+    pdl_wait();
     constexpr int RPP = RT / G;
     const int lane = threadIdx.x & 31, lig = lane & (G - 1), slot = threadIdx.x / G;
     const int d = a.dim, TR = a.tile_rows, N = a.bitwidth;
@@ -367,6 +371,7 @@ extern "C" int ds_restore_payload(const uint8_t *payload, const ds_restore_sec *
     if (per_sm < 1) per_sm = 1;
     const int64_t cap = (int64_t)host::sm_count() * per_sm;
     const int64_t grid = tiles < cap ? tiles : cap;
-    fn<<<(unsigned)grid, RT, smem, (cudaStream_t)stream>>>(a);
+    e = host::launch_pdl(fn, (unsigned)grid, (unsigned)RT, smem, (cudaStream_t)stream, a);
+    if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     return host::check_launch("ds_restore_payload");
 }
