@@ -171,6 +171,18 @@ __global__ void __launch_bounds__(MARK_THREADS) mark_kernel(const MarkArgs a, in
 #ifndef DS_MK_CACHE_BITS
 #define DS_MK_CACHE_BITS 13
 #endif
+#ifndef DS_MK_GRP_ROLLED
+#define DS_MK_GRP_ROLLED 0  // 1: packed id groups in a rolled loop (smaller code, A/B)
+#endif
+#ifndef DS_MK_WIN_SEQ
+#define DS_MK_WIN_SEQ 0  // 1: bit-window ids tested one at a time (A/B)
+#endif
+#ifndef DS_MK_PG
+// cache probes batched per lane (mode 2).  1 measured best (C2 K1 60 -> 48
+// µs): a batch reads its slots before updating them, so a repeated hot row
+// inside a batch sees a stale entry and issues a redundant RED
+#define DS_MK_PG 1
+#endif
 constexpr int MK_CACHE_BITS = DS_MK_CACHE_BITS;  // 2^13 entries = 64 KB (A/B: DS_MK_CACHE_BITS)
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -365,6 +377,15 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
                                  "r"(1) : "memory");
                 }
             }
+        } else if (mode == 1 && DS_MK_WIN_SEQ) {
+            // one id at a time: each test sees the bits the previous ids set
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                const bool ok = in_range(v[q]);
+                bad |= !ok;
+                const uint32_t bit = 1u << ((uint32_t)v[q] & 31);
+                if (ok && !(win[(uint32_t)v[q] >> 5] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
+            }
         } else if (mode == 1) {
             uint32_t cur[NQ];
             bool ok[NQ];
@@ -380,8 +401,8 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
                 if (!(cur[q] & bit)) atomicOr(win + ((uint32_t)v[q] >> 5), bit);
             }
         } else {
-            // probes in groups of 8 so their latencies overlap
-            constexpr int PG = NQ < 8 ? NQ : 8;
+            // probes in groups of DS_MK_PG (1: each probe sees the previous update)
+            constexpr int PG = NQ < DS_MK_PG ? NQ : DS_MK_PG;
 #pragma unroll
             for (int g = 0; g < NQ; g += PG) {
                 uint32_t w[PG], slot[PG];
@@ -413,7 +434,11 @@ __device__ __forceinline__ void mark_range(const MarkArgs &a, int seg, int64_t s
         if (j0 + PER_LANE <= cnt) {
             if constexpr (BITS) {
                 static_assert(PER_LANE % 8 == 0, "groups of 8 packed ids per lane");
+#if DS_MK_GRP_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
                 for (int grp = 0; grp < PER_LANE / 8; grp++) {
                     uint32_t v[8];
                     unpack8(reinterpret_cast<const uint32_t *>(stg), grp, v);
