@@ -39,6 +39,8 @@ def to_device(x, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
             t = t.to(dtype)
         return t.contiguous()
     a = np.ascontiguousarray(x, dtype=torch_to_numpy(dtype))
+    if not a.flags.writeable:  # torch.from_numpy warns on read-only views
+        a = a.copy()
     return torch.from_numpy(a).to(device, non_blocking=False)
 
 
