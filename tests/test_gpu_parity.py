@@ -249,12 +249,13 @@ def test_mark_batch_multi_table(ds, O):
 
 @pytest.mark.parametrize("dtype", (torch.int32, torch.int64))
 def test_mark_batch_table_kinds_and_bounds(ds, dtype):
-    """Every per-table K1 form (shared byte map <= 16352 rows, shared bit
-    window <= 65536 rows, cache + RED above), boundary sizes, Zipf-like
+    """Every per-table K1 form (shared byte map <= 65504 rows, shared bit
+    window <= 524288 rows, cache + RED above), boundary sizes, Zipf-like
     repeats, ragged segment tails; out-of-range ids raise BoundsError at the
     next sync and never leak a bit (the byte map's dummy byte at `rows`)."""
     rng = np.random.default_rng(11)
-    sizes = [1, 31, 32, 33, 1000, 16351, 16352, 16353, 65535, 65536, 65537, 300_001]
+    sizes = [1, 31, 32, 33, 1000, 16351, 16352, 16353, 65503, 65504, 65505, 65536, 65537,
+             300_001, 524_287, 524_288, 524_289, 3_000_001]
     rows = {t: r for t, r in enumerate(sizes)}
     tr = ds.ModelTracker(rows)
 
