@@ -96,6 +96,12 @@ def parse_args():
                    help="BASELINE.json config (C2 is the metric's headline config)")
     p.add_argument("--l2-fetch", type=int, default=64,
                    help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default)")
+    p.add_argument("--verify-rows", type=int, default=1_000_000,
+                   help="records of the last timed step's payload re-derived by the CPU oracle "
+                        "(plus every header, the whole dirty-id column, section ends and the "
+                        "records around byte 2^31 / 2^32); 0 = no parity check")
+    p.add_argument("--no-shipped", action="store_true",
+                   help="skip timing the reference package as shipped (baseline/_ref)")
     return p.parse_args()
 
 
@@ -192,6 +198,23 @@ def lookups_torch(kind, rows, n, gen, device):
     return perm[ranks].to(torch.int32)
 
 
+HOST_INPUT_BYTES = 8 << 30  # tables up to this size are drawn on the host (numpy)
+
+
+def table_bytes(w) -> int:
+    return int(sum(w["cards"])) * w["dim"] * 4
+
+
+def host_inputs(w, seed, rank=0):
+    """Tables U[-1, 1) (model.py:127-128) and the interval's lookups drawn with
+    numpy from (seed, rank): both arms of the bench (ours, --impl reference)
+    see the same bytes for the same rank."""
+    rng = np.random.default_rng([seed, rank])
+    tables = [(rng.random((r, w["dim"]), dtype=np.float32) * 2 - 1) for r in w["cards"]]
+    lookups = [lookups_numpy(w["lookups"], r, w["n_per_table"], rng) for r in w["cards"]]
+    return tables, lookups
+
+
 def lookups_numpy(kind, rows, n, rng):
     if kind == "uniform":
         return rng.integers(0, rows, n).astype(np.int32)
@@ -211,16 +234,21 @@ class CpuPath:
 
     Per step: DirtyBitmap.mark of every table's lookups (tracker.py:27-36),
     capture of the interval scope (tracker.py:54-58) + reset_interval
-    (:120-124), then build_shard_payload's incremental 8-bit section per
-    table (engine.py:139-187).  Tables run in parallel threads (ctypes
-    releases the GIL); rows of a section run on OpenMP threads.
+    (:120-124), then build_shard_payload's incremental section per table
+    (engine.py:139-187).  Tables run in parallel threads (ctypes releases the
+    GIL); rows of a section run on OpenMP threads.
+
+    tables: host arrays, or None with fetch(t, ids) for tables too large to
+    copy to the host (the T / C4 shards hold 64 GB): the sampled dirty rows
+    are then gathered before the timed build, which codes them in place.
     """
 
-    def __init__(self, tables, lookups, cards, threads, bitwidth=8, adaptive=None):
+    def __init__(self, tables, lookups, cards, threads, bitwidth=8, adaptive=None, fetch=None):
         from oracle import oracle as O
         self.bitwidth, self.adaptive = bitwidth, adaptive
         self.O = O
         self.tables, self.lookups, self.cards = tables, lookups, cards
+        self.fetch = fetch
         self.threads = threads
         self.bits = [np.zeros((r + 7) // 8, np.uint8) for r in cards]
         self.base = [np.zeros((r + 7) // 8, np.uint8) for r in cards]
@@ -253,29 +281,118 @@ class CpuPath:
             stride = int(np.ceil(rows / max_build_rows))
             ids = [i[::stride] for i in ids_all]
             scale = rows / max(1, sum(i.size for i in ids))
+        vals = None
+        if self.tables is None:  # untimed gather of the sampled rows from the device
+            vals = [self.fetch(t, ids[k]) for k, t in enumerate(ts)]
         big = [k for k, t in enumerate(ts) if ids[k].size > 65536]
         small = [k for k, t in enumerate(ts) if ids[k].size <= 65536]
 
         def build(k, nthreads):
             t = list(ts)[k]
+            if vals is not None:
+                return O.build_section(t, vals[k], None, bitwidth=self.bitwidth,
+                                       adaptive=self.adaptive, nthreads=nthreads)
             return O.build_section(t, self.tables[t], ids[k], bitwidth=self.bitwidth,
-                                   adaptive=self.adaptive,
-                                   nthreads=nthreads)
+                                   adaptive=self.adaptive, nthreads=nthreads)
 
+        t2 = time.perf_counter()
         outs = list(self.pool.map(lambda k: build(k, 1), small))
         for k in big:
             outs.append(build(k, self.threads))
-        t2 = time.perf_counter()
-        return rows, sum(len(o[0]) for o in outs), (t1 - t0) + (t2 - t1) * scale
+        t3 = time.perf_counter()
+        return rows, sum(len(o[0]) for o in outs), (t1 - t0) + (t3 - t2) * scale
 
 
-def cpu_measure(w, tables, lookups, budget_s=20.0, steps=None):
+def import_shipped_reference():
+    """The unmodified reference package from its offline install
+    (baseline/_ref, `pip install --no-index ... --target baseline/_ref`), or
+    None when it is not installed."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "deltasnap")):
+        return None
+    sys.dont_write_bytecode = True
+    if path not in sys.path:
+        sys.path.append(path)
+    try:
+        import deltasnap
+    except Exception:
+        return None
+    return deltasnap
+
+
+def shipped_measure(w, tables, lookups, payload=None, sample_rows=None, fetch=None):
+    """The reference as shipped: deltasnap's own
+    DirtyBitmap.mark + dirty_rows (tracker.py:27-58) over the interval's
+    lookups, then its build_shard_payload (engine.py:118-189) -- one shard,
+    so one writer thread (RunConfig.workers = shards, engine.py:231-233) --
+    over an evenly strided sample of the dirty rows, the build time scaled to
+    all of them (bytes are per-row, quant.py:14-15).  With `payload` (this
+    step's device-written payload, N = 1) the sampled records are compared
+    byte for byte with the reference's own.  tables=None: the sampled rows
+    are gathered from the device (fetch) before the timed build."""
+    ds_ref = import_shipped_reference()
+    if ds_ref is None:
+        return None
+    from types import SimpleNamespace
+    sample_rows = sample_rows or (20_000 if w["adaptive"] else 100_000)
+    t0 = time.perf_counter()
+    ids = []
+    for t, (r, lk) in enumerate(zip(w["cards"], lookups)):
+        bm = ds_ref.tracker.DirtyBitmap(t, r)
+        bm.mark(lk)
+        ids.append(bm.dirty_rows()[0])
+    t_track = time.perf_counter() - t0
+    total = sum(i.size for i in ids)
+    stride = max(1, int(np.ceil(total / sample_rows)))
+    sel = [i[::stride] for i in ids]
+    n_sel = sum(x.size for x in sel)
+    if tables is None:  # the sampled rows only, as a table of their own
+        tabs = [fetch(t, sel[t]) for t in range(len(sel))]
+        rows = {t: np.arange(sel[t].size, dtype=np.int64) for t in range(len(sel))}
+    else:
+        tabs, rows = tables, dict(enumerate(sel))
+    snap = SimpleNamespace(shard_tables=lambda sid: [
+        ds_ref.model.EmbeddingTable(t, v) for t, v in enumerate(tabs)])
+    plan = ds_ref.policy.CheckpointPlan(kind="incremental", rows=rows, bitwidth=w["bitwidth"])
+    overrides = None if w["adaptive"] else {w["bitwidth"]: None}
+    t1 = time.perf_counter()
+    blob, _, _ = ds_ref.engine.build_shard_payload(snap, plan, 0, 1024, overrides)
+    t_build = (time.perf_counter() - t1) * total / max(1, n_sel)
+    secs = t_track + t_build
+    out = {"value": total * w["dim"] * 4 / secs / 1e9, "unit": "GB/s", "cores": 1,
+           "kind": "reference", "rows_per_s": total / secs,
+           "sample": f"deltasnap (baseline/_ref) as shipped, one writer thread: mark + dirty_rows "
+                     f"of all {sum(len(l) for l in lookups)} lookups ({t_track:.2f} s), "
+                     f"build_shard_payload of every {stride}-th dirty row ({n_sel} rows, "
+                     f"{time.perf_counter() - t1:.2f} s, scaled to {total})"}
+    if payload is not None:
+        # the reference's records vs the same records of our payload (ids
+        # excluded when the sampled rows were re-based into their own table)
+        rec = 16 + (w["dim"] * w["bitwidth"] + 7) // 8
+        skip = 8 if tables is None else 0
+        ref_b = np.frombuffer(blob, np.uint8)
+        off_r, off_p, bad, n = 0, 0, 0, 0
+        for i in ids:
+            pos = np.arange(0, i.size, stride)
+            ours = payload[off_p + 24: off_p + 24 + i.size * rec].reshape(i.size, rec)[pos, skip:]
+            theirs = ref_b[off_r + 24: off_r + 24 + pos.size * rec].reshape(pos.size, rec)[:, skip:]
+            bad += int(np.any(ours != theirs, axis=1).sum())
+            n += pos.size
+            off_p += 24 + i.size * rec
+            off_r += 24 + pos.size * rec
+        out["parity_vs_shipped"] = {"records_compared": n, "mismatches": bad,
+                                    "ids_compared": skip == 0}
+    return out
+
+
+def cpu_measure(w, tables, lookups, budget_s=20.0, steps=None, shipped=False, payload=None,
+                fetch=None):
     """The reference CPU path (oracle port) on all host threads: GB/s of
     checkpointed rows over whole intervals (C2) or, for the large workloads,
     intervals whose section build is sampled to ~budget_s."""
     threads = os.cpu_count() or 1
     acfg = {2: (25, 0.5), 3: (25, 0.2), 4: (45, 0.2)}.get(w["bitwidth"]) if w["adaptive"] else None
-    cp = CpuPath(tables, lookups, w["cards"], threads, w["bitwidth"], acfg)
+    cp = CpuPath(tables, lookups, w["cards"], threads, w["bitwidth"], acfg, fetch=fetch)
     big = sum(w["cards"]) > 50_000_000 or w["adaptive"]
     cap = (200_000 if w["adaptive"] else 2_000_000) if big else None
     cp.step(max_build_rows=cap)  # warm-up (page-in, OpenMP pool)
@@ -290,9 +407,14 @@ def cpu_measure(w, tables, lookups, budget_s=20.0, steps=None):
     sample = (f"{reps} full interval(s): mark {int(sum(len(l) for l in lookups))} lookups, "
               f"capture, {'adaptive' if w['adaptive'] else 'naive'} {w['bitwidth']}-bit sections of "
               + ("every dirty row" if cap is None else f"a strided sample of {cap} dirty rows "
-                 "(build time scaled to all dirty rows)"))
-    return {"value": rows_c * w["dim"] * 4 / secs / 1e9, "unit": "GB/s", "cores": threads,
-            "kind": "port", "sample": sample, "seconds": secs, "steps": reps}
+                 "(build time scaled to all dirty rows"
+                 + (", the sampled rows gathered from the device table before the build)"
+                    if tables is None else ")")))
+    out = {"value": rows_c * w["dim"] * 4 / secs / 1e9, "unit": "GB/s", "cores": threads,
+           "kind": "port", "sample": sample, "seconds": secs, "steps": reps}
+    if shipped:
+        out["reference_as_shipped"] = shipped_measure(w, tables, lookups, payload, fetch=fetch)
+    return out
 
 
 def pack_lookups(lookups, cards, dev):
@@ -313,22 +435,85 @@ def run_reference(args):
     if rank != 0:
         return
     w = workload_of(args)
-    cards = w["cards"]
-    rng = np.random.default_rng(args.seed)
-    tables = [(rng.random((r, w["dim"]), dtype=np.float32) * 2 - 1) for r in cards]
-    lookups = [lookups_numpy(w["lookups"], r, w["n_per_table"], rng) for r in cards]
-    cpu = cpu_measure(w, tables, lookups, steps=max(1, args.steps))
+    if table_bytes(w) <= HOST_INPUT_BYTES:
+        tables, lookups = host_inputs(w, args.seed, 0)
+        fetch, input_gen = None, "numpy default_rng([seed, rank]) (same draw as --impl reference)"
+    else:
+        # 64 GB shards: only the sampled dirty rows are materialised (random
+        # U[-1, 1) rows per request); the lookups are the full interval's
+        rng = np.random.default_rng([args.seed, 0])
+        lookups = [lookups_numpy(w["lookups"], r, w["n_per_table"], rng) for r in w["cards"]]
+        tables = None
+
+        def fetch(t, ids):
+            return np.random.default_rng([args.seed, t, len(ids)]).random(
+                (len(ids), w["dim"]), dtype=np.float32) * 2 - 1
+        input_gen = "torch.Generator on the device"
+    dirty = sum(np.unique(lk).size for lk in lookups)
+    cpu = cpu_measure(w, tables, lookups, steps=max(1, args.steps), fetch=fetch,
+                      shipped=not args.no_shipped)
     value = cpu["value"]
+    world = max(1, args.gpus)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": cpu["steps"], "warmup": 1,
         "ms_per_step": cpu["seconds"] / cpu["steps"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
-        "config": workload_desc(w),
-        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "config": dict(workload_desc(w), dirty_rows_per_step=dirty * world,
+                       parallelism=f"row-sharded x{world}", inputs=input_gen,
+                       **({"rank_alignment": "device all_reduce after each untimed L2 flush"}
+                          if world > 1 else {})),
+        "cpu_baseline": dict({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                             reference_as_shipped=cpu.get("reference_as_shipped")),
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def step_payload(ck, host_payload, local):
+    """This rank's payload of one step as a CNR1 payload: N = 1 writes whole
+    sections; N > 1 writes bare record runs, which get headers with the
+    rank's own counts here (the assembled shard is the rank-order
+    concatenation of such runs, sharded.assemble_shard)."""
+    if ck.world == 1:
+        return host_payload
+    from paper_2010_08679_b200.payload import pack_header
+    parts, off = [], 0
+    for t, n in zip(ck.tables, local):
+        parts.append(np.frombuffer(pack_header(t.table_id, int(n), t.dim, ck.bitwidth,
+                                               1 if ck.bitwidth else 0, False), np.uint8))
+        parts.append(host_payload[off:off + int(n) * ck.rec])
+        off += int(n) * ck.rec
+    return np.concatenate(parts)
+
+
+def verify_step(ck, tables, look_host, w, host_payload, local, sample):
+    """Checks one step's payload against the CPU oracle (oracle/verify.py):
+    every header, the whole dirty-id column (= np.unique of the interval's
+    lookups, tracker.py:54-58), and `sample` strided records plus section
+    ends and the records around byte 2^31 / 2^32 re-derived from the same
+    table rows (engine.py:118-189)."""
+    import torch
+    from oracle.verify import verify_payload
+    exp = []
+    for t, lk in zip(tables, look_host):
+        exp.append(dict(table_id=t.table_id, dim=t.dim, ids=np.unique(lk).astype(np.int64) + t.row_base))
+    by_id = {t.table_id: t for t in tables}
+
+    def fetch(tid, ids):
+        t = by_id[tid]
+        idx = torch.from_numpy(np.asarray(ids, np.int64) - t.row_base).to(t.values.device)
+        return t.values.index_select(0, idx).cpu().numpy()
+
+    adaptive = None
+    if w["adaptive"]:
+        adaptive = {2: (25, 0.5), 3: (25, 0.2), 4: (45, 0.2)}[w["bitwidth"]]
+    r = verify_payload(step_payload(ck, host_payload, local), exp, bitwidth=w["bitwidth"],
+                       adaptive=adaptive, incremental=True, fetch_rows=fetch, sample=sample)
+    r["checked_against"] = ("CPU oracle (oracle/deltasnap_oracle.c) re-deriving the records from "
+                            "the same table rows; ids against np.unique of the lookups")
+    r["rows_checked"] = r["records_checked"]
+    return r
 
 
 def run_ours(args):
@@ -356,13 +541,25 @@ def run_ours(args):
     w = workload_of(args)
     cards, DIM = w["cards"], w["dim"]
     n_look = w["n_per_table"]
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(args.seed * 7919 + rank)
     tables = []
-    for t, r in enumerate(cards):
-        v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
-        tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
-    lookups = [lookups_torch(w["lookups"], r, n_look, gen, dev) for r in cards]
+    if table_bytes(w) <= HOST_INPUT_BYTES:
+        # the same numpy draw as --impl reference (identical inputs per rank)
+        h_tables, h_look = host_inputs(w, args.seed, rank)
+        for t, (r, v) in enumerate(zip(cards, h_tables)):
+            tables.append(ds.DeviceTable(t, torch.from_numpy(v).to(dev), row_base=rank * r,
+                                         total_rows=world * r))
+        lookups = [torch.from_numpy(lk).to(dev) for lk in h_look]
+        del h_tables, h_look
+        input_gen = "numpy default_rng([seed, rank]) (same draw as --impl reference)"
+    else:
+        # 64 GB shards: drawn on the device (Philox)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(args.seed * 7919 + rank)
+        for t, r in enumerate(cards):
+            v = torch.rand((r, DIM), generator=gen, device=dev, dtype=torch.float32).mul_(2).sub_(1)
+            tables.append(ds.DeviceTable(t, v, row_base=rank * r, total_rows=world * r))
+        lookups = [lookups_torch(w["lookups"], r, n_look, gen, dev) for r in cards]
+        input_gen = "torch.Generator on the device"
     # the interval's lookup stream, each table's ids at ceil(log2(rows))
     # bits: ds_mark_packed's input (host copy for e2e, device copy in HBM)
     host_stream, stream = pack_lookups(lookups, cards, dev)
@@ -456,6 +653,13 @@ def run_ours(args):
     value = dirty_all * row_bytes * K / elapsed / 1e9
     _ = ck.fetch()  # error flags of the timed steps
 
+    # ---- parity of the last timed step's payload at full scale (oracle as checker) ------
+    look_host = [lk.cpu().numpy() for lk in lookups]
+    parity, host_payload = None, None
+    if args.verify_rows > 0:
+        host_payload = ck.payload[:nbytes].cpu().numpy()
+        parity = verify_step(ck, tables, look_host, w, host_payload, local, args.verify_rows)
+
     # roofline of the dominant kernel (algorithmic bytes / its mean duration)
     rec = ck.rec
     k1_bytes = stream.nbytes
@@ -545,38 +749,77 @@ def run_ours(args):
     # lookups come from pinned host memory (H2D) and each step's payload goes
     # back to pinned host memory (D2H); copies overlap the kernels of the
     # neighbouring steps on their own streams.  Timed on the host clock
-    # (the pipeline synchronises on the host between steps).
+    # (the pipeline synchronises on the host between steps).  Headline: the
+    # lookups as a data loader emits them -- int32 row ids per table
+    # (DirtyBitmap.mark's input, tracker.py:27-36), K1 = ds_mark over the
+    # concatenation; secondary: the bit-packed LookupStream (packed on the
+    # host once, outside the timed region).
     e2e = None
     if not args.no_e2e:
         from paper_2010_08679_b200.pipeline import CheckpointPipeline
-        pipe = CheckpointPipeline(ck, host_stream.nbytes, torch.uint8)
-        for _ in range(3):
-            pipe.submit(host_stream)
-        pipe.drain()
-        h2d0, d2h0 = pipe.h2d_bytes, pipe.d2h_bytes
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(K):
-            pipe.submit(host_stream)
-        pipe.drain()
-        e_el = max_over_ranks(time.perf_counter() - t0)
-        barrier()
-        e2e = {"value": dirty_all * row_bytes * K / e_el / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": int((pipe.h2d_bytes - h2d0) / K),
-               "d2h_bytes_per_step": int((pipe.d2h_bytes - d2h0) / K),
-               "ms_per_step": e_el / K * 1e3,
-               "overlap": "H2D(k+1) | kernels(k) | D2H(k-1) on separate streams"}
-        ck.payload = pipe.payload[0]
+        seg_off = np.concatenate([[0], np.cumsum([lk.size for lk in look_host])]).astype(np.int64)
+        seg_tab = np.arange(len(look_host), dtype=np.int64)
+        host_i32 = torch.from_numpy(np.concatenate(look_host).astype(np.int32)).pin_memory()
+
+        def e2e_run(feed, cap, dtype, steps):
+            pipe = CheckpointPipeline(ck, cap, dtype)
+            for _ in range(3):
+                feed(pipe)
+            pipe.drain()
+            h2d0, d2h0 = pipe.h2d_bytes, pipe.d2h_bytes
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                feed(pipe)
+            pipe.drain()
+            el = max_over_ranks(time.perf_counter() - t0)
+            barrier()
+            out = {"value": dirty_all * row_bytes * steps / el / 1e9, "unit": "GB/s",
+                   "h2d_bytes_per_step": int((pipe.h2d_bytes - h2d0) / steps),
+                   "d2h_bytes_per_step": int((pipe.d2h_bytes - d2h0) / steps),
+                   "ms_per_step": el / steps * 1e3}
+            ck.payload = pipe.payload[0]
+            return out
+
+        e2e = e2e_run(lambda p: p.submit(host_i32, seg_off, seg_tab), host_i32.numel(),
+                      torch.int32, K)
+        e2e.update(lookups="int32 row ids per table, pinned host memory (106 B per C2 batch "
+                           "position of 26 lookups)" if args.workload == "C2" else
+                           "int32 row ids per table, pinned host memory",
+                   overlap="H2D(k+1) | kernels(k) | D2H(k-1) on separate streams")
+        packed = e2e_run(lambda p: p.submit(host_stream), host_stream.nbytes, torch.uint8, K)
+        packed["lookups"] = ("LookupStream: ids bit-packed at ceil(log2 rows) bits, packed on "
+                             "the host outside the timed region")
+        e2e["packed_stream"] = packed
+        # the pipeline's own D2H'd payloads (double-buffered slots) of 3
+        # consecutive steps are the verified payload, byte for byte
+        if host_payload is not None:
+            pipe = CheckpointPipeline(ck, host_i32.numel(), torch.int32, keep_outputs=True)
+            for _ in range(3):
+                pipe.submit(host_i32, seg_off, seg_tab)
+            outs = pipe.drain()
+            ck.payload = pipe.payload[0]
+            same = sum(1 for o in outs if o == host_payload.tobytes())
+            parity["pipeline_payloads_equal"] = f"{same}/{len(outs)}"
+            if same != len(outs):
+                parity["mismatches"] += len(outs) - same
 
     # ---- CPU baseline (rank 0, N == 1): oracle port on the same inputs ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        host_tables = [t.values.cpu().numpy() for t in tables]
-        host_look = [lk.cpu().numpy() for lk in lookups]
         del lookups
-        c = cpu_measure(w, host_tables, host_look)
+        big = sum(t.values.numel() for t in tables) * 4 > (8 << 30)
+        host_tables = None if big else [t.values.cpu().numpy() for t in tables]
+
+        def fetch(t, ids):
+            tv = tables[t].values
+            return tv.index_select(0, torch.from_numpy(np.asarray(ids, np.int64)).to(dev)).cpu().numpy()
+
+        c = cpu_measure(w, host_tables, look_host, shipped=not args.no_shipped,
+                        payload=host_payload, fetch=fetch)
         cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu["reference_as_shipped"] = c.get("reference_as_shipped")
 
     if rank == 0:
         line = {
@@ -584,14 +827,17 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": elapsed / K * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
             "config": dict(workload_desc(w), dirty_rows_per_step=dirty_all,
-                           parallelism=f"row-sharded x{world}", l2_fetch_bytes=l2_fetch,
+                           parallelism=f"row-sharded x{world}", inputs=input_gen,
                            **({"rank_alignment": "device all_reduce after each untimed L2 flush"}
                               if world > 1 else {})),
+            "l2_fetch_bytes": l2_fetch,
             "rows_per_s": dirty_all * K / elapsed,
             "roofline": roofline, "phases": phases, "payload_crc32": crc, "staged": staged,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
-            # per step: mark_tma 1 + cap3 count/scan/emit 3 + layout/writer/err_reduce 3
-            "gpu_launches": K * 7,
+            "parity": parity,
+            # per timed step: mark_tma 1 + cap3_count 1 + cap3_emit 1 + writer 1 (the
+            # layout, the count exchange and the error sum run inside the writer)
+            "gpu_launches": K * 4,
             "payload_bytes_per_step": int(nbytes) if world == 1 else None,
         }
         print(json.dumps(line), flush=True)
@@ -700,6 +946,31 @@ def run_restore(args):
             times_e2e.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     te = float(np.mean(times_e2e))
+
+    # parity: every restored row (and the rebuilt since-baseline bits) against
+    # the CPU oracle applying the same chain (engine.py:459-485)
+    parity = None
+    if args.verify_rows > 0:
+        from oracle import oracle as O
+        t0 = time.perf_counter()
+        split = [(kind != "full", dict(O.split_sections(h, kind != "full"))) for kind, h in host]
+        rows_ok = rows_n = bits_bad = 0
+        for tb in tables:
+            tid = tb.table_id
+            want = np.zeros((tb.rows, dim), np.float32)
+            bits = np.zeros((tb.rows + 7) // 8, np.uint8)
+            for inc, secs in split:
+                if tid in secs:
+                    O.apply_section(secs[tid], inc, want, None, bits if inc else None)
+            got = out[tid].values.cpu().numpy()
+            rows_ok += int(np.all(got.view(np.uint32) == want.view(np.uint32), axis=1).sum())
+            rows_n += tb.rows
+            bits_bad += int(not np.array_equal(base[tid].to_bytes(), bits))
+        parity = {"rows_checked": rows_n, "mismatches": rows_n - rows_ok + bits_bad,
+                  "baseline_bitmaps_checked": len(tables),
+                  "checked_against": "CPU oracle applying the same chain (every row of every "
+                                     "table, bit-exact float32; since-baseline bits)",
+                  "seconds": time.perf_counter() - t0}
     nbytes = rows_restored * dim * 4
     h2d = sum(p.numel() for p in pinned)
     # roofline: the restore kernels' algorithmic bytes = chain bytes read +
@@ -720,6 +991,7 @@ def run_restore(args):
                      "frac": alg / t / 1e9 / peak, "traffic": None},
         "e2e": {"value": nbytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4 * len(host) * 26},
+        "parity": parity,
         "clocks": clocks.summary(), "gpu_launches": K * sum(restore_launches(h, kind != "full")
                                                          for (kind, h) in host),
     }

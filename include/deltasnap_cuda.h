@@ -181,6 +181,9 @@ typedef struct {
     const struct ds_peer_exchange *exchange; /* NULL, or the row-sharded count exchange run
                                   inside this launch (below): CTA 0 publishes, the last
                                   CTA waits for every rank and writes exchange->out */
+    int64_t staged_rows;       /* capacity of `staged` in rows: a larger dirty total sets
+                                  DS_FLAG_CAPACITY and writes no records (like the payload
+                                  capacity) instead of reading past the staging buffer */
 } ds_ckpt_params;
 
 /* Counters of the certified fast path (diagnostics). */

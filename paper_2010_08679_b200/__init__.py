@@ -50,7 +50,12 @@ from .payload import (
     serialize_shard_payload,
 )
 from .engine import (
+    DeviceModelConfig,
+    DeviceModelState,
     DeviceTable,
+    IntervalSizes,
+    ReaderPosition,
+    RestoredRun,
     RestoredTables,
     ShardWriter,
     apply_payload,
@@ -58,6 +63,7 @@ from .engine import (
     restore,
     restore_chain,
     stage_chain,
+    state_digest,
 )
 
 __version__ = "0.1.0"

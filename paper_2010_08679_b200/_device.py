@@ -20,8 +20,15 @@ def device_of(dev=None) -> torch.device:
     dev = torch.device(dev)
     if dev.type != "cuda":
         raise ValueError(f"paper_2010_08679_b200 runs on CUDA devices only, got {dev}")
+    cur = torch.cuda.current_device()
     if dev.index is None:
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = torch.device("cuda", cur)
+    elif dev.index != cur:
+        # the entry points launch on the current device's stream (and the C
+        # side caches per-device properties of cudaGetDevice): refuse a launch
+        # that would pair another device's pointers with this device
+        raise ValueError(f"paper_2010_08679_b200: {dev} is not the current device cuda:{cur}; "
+                         "call torch.cuda.set_device() or run under torch.cuda.device()")
     return dev
 
 

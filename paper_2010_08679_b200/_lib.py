@@ -69,6 +69,7 @@ class CkptParams(ctypes.Structure):
         ("stats", ctypes.c_void_p),
         ("staged", ctypes.c_void_p),
         ("exchange", ctypes.c_void_p),
+        ("staged_rows", ctypes.c_int64),
     ]
 
 

@@ -219,9 +219,12 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     a.flags = flags;
     a.stats = p->stats;
     a.staged = p->staged;
+    a.staged_rows = p->staged ? p->staged_rows : 0;
     if (p->staged && (!p->incremental || !p->ids_packed || p->aux || (mode_of(p) == 2 && DS_GREEDY_CTA)))
         return host::fail(DS_ERR_ARG, "ds_write_payload: staged rows need an incremental "
                                       "checkpoint with packed ids and no aux");
+    if (p->staged && p->staged_rows < 0)
+        return host::fail(DS_ERR_ARG, "ds_write_payload: negative staged_rows");
 
     a.has_x = p->exchange != nullptr;
     if (a.has_x) {

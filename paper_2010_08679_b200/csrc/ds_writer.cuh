@@ -53,6 +53,7 @@ struct WriterArgs {
     uint32_t *flags;
     unsigned long long *stats;
     const float *staged;  // rows gathered by ds_stage_rows (read record i of the packed order)
+    int64_t staged_rows;  // capacity of staged in rows (a larger dirty total: flagged, nothing written)
     int has_x;            // the row-sharded count exchange runs in this launch
     ds_peer_exchange x;
 };
@@ -120,6 +121,10 @@ __device__ __forceinline__ void peer_wait(const WriterArgs &a) {
         if (lane == 0) atomicOr(x.flags, DS_FLAG_TIMEOUT);
         return;
     }
+    // lane r's acquire orders only lane r's later loads: a system-scope
+    // acquire fence makes every rank's slot writes visible to every lane
+    __syncwarp();
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     const volatile int64_t *slots =
         reinterpret_cast<const int64_t *>(local + peer_flags_bytes(x.world)) + (size_t)par * x.world * n;
     for (int i = lane; i < x.world * n; i += 32) x.out[i] = slots[i];
@@ -468,12 +473,17 @@ __device__ __forceinline__ void writer_layout(const WriterArgs &a, int64_t *s_sc
         }
         if (lane == 0) {
             s_sched[nt] = tiles0;
+            s_sched[3 * nt + 1] = ids0;  // records of the call
             s_sec[nt] = off0;
         }
     }
     __syncthreads();
     if (blockIdx.x == 0) {
         const int64_t total = s_sec[nt];
+        // a staged write whose dirty total exceeds the staging buffer would
+        // read rows stage_rows never wrote: flagged, no records written
+        if (threadIdx.x == 0 && a.staged && s_sched[3 * nt + 1] > a.staged_rows)
+            atomicOr(a.flags, DS_FLAG_CAPACITY);
         // the last warp publishes this rank's counts to the peers (its fence
         // delays only that warp)
         if (a.has_x && (threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1) peer_publish(a, s_sched);
@@ -495,6 +505,14 @@ __device__ __forceinline__ void writer_layout(const WriterArgs &a, int64_t *s_sc
             }
         }
     }
+}
+
+// the records fit the payload (and, staged, the staging buffer); else flagged
+// by CTA 0 and nothing but the headers is written
+__device__ __forceinline__ bool writer_fits(const WriterArgs &a, const int64_t *s_sched,
+                                            const int64_t *s_sec) {
+    const int nt = a.ntables;
+    return s_sec[nt] <= a.capacity && (!a.staged || s_sched[3 * nt + 1] <= a.staged_rows);
 }
 
 // block-level epilogue: error partial, flags, diagnostics; the last CTA to
@@ -821,7 +839,7 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
     writer_layout(a, s_sched, s_sec);
     const int nt = a.ntables;
     WAcc acc;
-    if (s_sec[nt] <= a.capacity) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
+    if (writer_fits(a, s_sched, s_sec)) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
         const int64_t total_tiles = s_sched[nt];
         const int nwc = blockDim.x >> 5;  // warps per CTA (fewer for huge records)
         const int64_t gw = (int64_t)blockIdx.x * nwc + wid;
@@ -1017,7 +1035,7 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
     const int lane = threadIdx.x & 31;
     const int lig = lane & (G - 1);
     const int slot = threadIdx.x / G;
-    if (s_sec[nt] <= a.capacity) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
+    if (writer_fits(a, s_sched, s_sec)) {  // else flagged (DS_FLAG_CAPACITY) by CTA 0
         const int64_t total_tiles = s_sched[nt];
         for (int64_t tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const int t = tile_table(s_sched, nt, tile, lane);

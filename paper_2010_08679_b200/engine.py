@@ -167,6 +167,7 @@ class ShardWriter:
         self.params.ids_local = int(local_ids)
         # rows gathered by stage_rows (packed id order) instead of the live tables
         self.params.staged = staged.data_ptr() if staged is not None else None
+        self.params.staged_rows = int(staged.shape[0]) if staged is not None else 0
         self.params.exchange = ctypes.addressof(exchange) if exchange is not None else None
         if incremental and ids_offsets is not None:
             for k in range(len(self.tables)):
@@ -440,54 +441,282 @@ def stage_chain(chain: list, checksums: list | None = None, device=None) -> list
     return staged
 
 
+# ---------------------------------------------------------------------------
+# what restore() returns: the reference's RestoredRun (engine.py:415-425) with
+# the tables resident in HBM
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DeviceModelConfig:
+    """ModelConfig (model.py:18-40) as config_from_manifest (engine.py:427-440)
+    derives it.  The reference raises IntegrityError for mixed table shapes;
+    the device restore allows them (Criteo-shaped tables): rows_per_table and
+    dim are then None and `shapes` holds every table's (rows, dim)."""
+
+    num_tables: int
+    rows_per_table: int | None
+    dim: int | None
+    num_shards: int = 1
+    has_aux_state: bool = False
+    dense_dim: int = 256
+    shapes: dict = field(default_factory=dict)
+
+    def validate(self) -> None:
+        """model.py:27-37 (ConfigError), per table for mixed shapes."""
+        if self.num_tables < 1:
+            raise ConfigError("num_tables must be >= 1")
+        if any(r < 1 for r, _ in self.shapes.values()):
+            raise ConfigError("rows_per_table must be >= 1")
+        if any(d < 1 for _, d in self.shapes.values()):
+            raise ConfigError("dim must be >= 1")
+        if self.num_shards < 1:
+            raise ConfigError("num_shards must be >= 1")
+        if self.dense_dim < 1:
+            raise ConfigError("dense_dim must be >= 1")
+
+    def shard_of(self, table_id: int) -> int:
+        return table_id % self.num_shards  # model.py:39-40
+
+
+@dataclass
+class ReaderPosition:
+    """ReaderState (model.py:67-80)."""
+
+    batches_consumed: int = 0
+    rng_cursor: int = 0
+
+    def copy(self) -> "ReaderPosition":
+        return ReaderPosition(self.batches_consumed, self.rng_cursor)
+
+
+@dataclass
+class DeviceModelState:
+    """ModelState (model.py:83-98) with DeviceTable tables.  shard_tables()
+    has the reference's meaning, so a restored model feeds
+    build_shard_payload directly."""
+
+    config: DeviceModelConfig
+    tables: dict
+    dense: np.ndarray
+    reader: ReaderPosition = field(default_factory=ReaderPosition)
+
+    def shard_tables(self, shard_id: int) -> list:
+        return [t for tid, t in sorted(self.tables.items())
+                if self.config.shard_of(tid) == shard_id]
+
+    def host_tables(self) -> dict:
+        """{tid: (values, aux | None)} as float32 numpy arrays (D2H)."""
+        return {tid: (t.values.cpu().numpy(), None if t.aux is None else t.aux.cpu().numpy())
+                for tid, t in sorted(self.tables.items())}
+
+
+@dataclass
+class IntervalSizes:
+    """IntervalHistory (policy.py:23-44): increment sizes as fractions of the
+    baseline's bytes, clamped to 1.0."""
+
+    sizes: list = field(default_factory=list)
+
+    def record(self, fraction: float) -> None:
+        import math
+
+        from .errors import DataError
+        if not math.isfinite(fraction) or fraction < 0.0:
+            raise DataError(f"invalid increment fraction {fraction!r}")
+        self.sizes.append(min(fraction, 1.0))
+
+    def reset(self) -> None:
+        self.sizes.clear()
+
+    def __len__(self) -> int:
+        return len(self.sizes)
+
+
+@dataclass
+class RestoredRun:
+    """Everything needed to resume training from a committed checkpoint
+    (engine.py:415-425): same fields, tables in HBM, tracker on the device
+    with the since-baseline scope rebuilt (engine.py:476)."""
+
+    model: DeviceModelState
+    tracker: object
+    history: IntervalSizes
+    baseline_id: int
+    baseline_payload_bytes: int
+    manifest: object
+    chain_ids: list
+
+    # pre-RestoredRun field names (restore_chain's RestoredTables)
+    @property
+    def tables(self) -> dict:
+        return self.model.tables
+
+    @property
+    def dense(self) -> np.ndarray:
+        return self.model.dense
+
+    def to_reference(self, deltasnap, tracker: str = "device"):
+        """The reference's own RestoredRun over host copies, for code that
+        needs numpy tables (sim.apply_batch, state_digest): `deltasnap` is
+        the reference package; tracker="device" keeps this tracker (a drop-in
+        for deltasnap.tracker.ModelTracker), "reference" copies the rebuilt
+        since-baseline bits into a reference ModelTracker."""
+        M = deltasnap.model
+        cfg = self.model.config
+        if cfg.rows_per_table is None:
+            raise IntegrityError("tables with mixed shapes are not supported")
+        tables = {tid: M.EmbeddingTable(tid, v, a)
+                  for tid, (v, a) in self.model.host_tables().items()}
+        model = M.ModelState(
+            config=M.ModelConfig(num_tables=cfg.num_tables, rows_per_table=cfg.rows_per_table,
+                                 dim=cfg.dim, num_shards=cfg.num_shards,
+                                 has_aux_state=cfg.has_aux_state, dense_dim=cfg.dense_dim),
+            tables=tables, dense=self.model.dense.copy(),
+            reader=M.ReaderState(self.model.reader.batches_consumed, self.model.reader.rng_cursor))
+        tr = self.tracker
+        if tracker == "reference":
+            tr = deltasnap.tracker.ModelTracker({tid: t.rows for tid, t in tables.items()})
+            for tid in tables:
+                tr.mark_baseline(tid, self.tracker.baseline_bitmap(tid).dirty_rows()[0])
+        hist = deltasnap.policy.IntervalHistory()
+        hist.sizes.extend(self.history.sizes)
+        return deltasnap.engine.RestoredRun(
+            model=model, tracker=tr, history=hist, baseline_id=self.baseline_id,
+            baseline_payload_bytes=self.baseline_payload_bytes, manifest=self.manifest,
+            chain_ids=list(self.chain_ids))
+
+
+def state_digest(state) -> str:
+    """model.py:156-165: SHA-256 over every table (values, then aux) in table
+    order, then the dense vector -- for device or host models."""
+    import hashlib
+    h = hashlib.sha256()
+    for tid in sorted(state.tables):
+        t = state.tables[tid]
+        for a in (t.values, t.aux):
+            if a is None:
+                continue
+            a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+            h.update(np.ascontiguousarray(a).tobytes())
+    dense = state.dense.cpu().numpy() if isinstance(state.dense, torch.Tensor) else state.dense
+    h.update(np.ascontiguousarray(dense).tobytes())
+    return h.hexdigest()
+
+
+def _dense_from_bytes(data: bytes, dense_dim: int) -> np.ndarray:
+    """engine.py:196-199"""
+    from .errors import FormatError
+    if len(data) != dense_dim * 4:
+        raise FormatError(f"dense payload has {len(data)} bytes, expected {dense_dim * 4}")
+    return np.frombuffer(data, dtype="<f4").astype(np.float32)
+
+
+def _config_from_manifest(target) -> DeviceModelConfig:
+    """engine.py:427-440, mixed shapes allowed (see DeviceModelConfig)."""
+    shapes = {tid: (int(info.rows), int(info.dim)) for tid, info in target.tables.items()}
+    rows = {r for r, _ in shapes.values()}
+    dims = {d for _, d in shapes.values()}
+    return DeviceModelConfig(
+        num_tables=len(shapes),
+        rows_per_table=rows.pop() if len(rows) == 1 else None,
+        dim=dims.pop() if len(dims) == 1 else None,
+        num_shards=len(target.shards), has_aux_state=bool(target.aux),
+        dense_dim=target.dense.nbytes // 4, shapes=shapes)
+
+
+def _verify_presence(cstore, chain) -> None:
+    """store.verify (store.py:488-501) minus the shard checksums, which
+    stage_chain checks on the device: presence and size of every object, and
+    the dense objects' CRC32 on the host (a few KB)."""
+    import zlib
+    for m in chain:
+        for e in list(m.shards.values()) + [m.dense]:
+            try:
+                data = cstore.store.get(e.key)
+            except KeyError:
+                raise IntegrityError(f"missing object {e.key!r}") from None
+            if len(data) != e.nbytes:
+                raise IntegrityError(f"size mismatch for {e.key!r}: {len(data)} != {e.nbytes}")
+            if e is m.dense and (zlib.crc32(data) & 0xFFFFFFFF) != (int(e.crc32) & 0xFFFFFFFF):
+                raise IntegrityError(f"checksum mismatch for {e.key!r}")
+
+
+def _restore_at(cstore, ckpt_id: int, device=None, verify_on_device: bool = False,
+                row_range: tuple | None = None) -> RestoredRun:
+    """engine.py:443-512 with the decode + scatter on the GPU."""
+    if verify_on_device:
+        chain = cstore.resolve_chain(ckpt_id)
+        _verify_presence(cstore, chain)
+    else:
+        chain = cstore.verify_chain(ckpt_id)
+    base, target = chain[0], chain[-1]
+    config = _config_from_manifest(target)
+    config.validate()
+    plan = [(m.kind, [cstore.store.get(e.key) for _, e in sorted(m.shards.items())])
+            for m in chain]
+    if verify_on_device:
+        sums = [[e.crc32 for _, e in sorted(m.shards.items())] for m in chain]
+        plan = stage_chain(plan, sums, device=device)
+    out = restore_chain(plan, config.shapes, aux=bool(target.aux), device=device,
+                        row_range=row_range)
+    dense = _dense_from_bytes(cstore.store.get(target.dense.key), config.dense_dim)
+    model = DeviceModelState(config=config, tables=out.tables, dense=dense,
+                             reader=ReaderPosition(target.reader_batches, target.reader_cursor))
+    # engine.py:495-502
+    history = IntervalSizes()
+    if base.payload_bytes > 0:
+        for mid in cstore.valid_ids():
+            if mid <= base.checkpoint_id or mid > target.checkpoint_id:
+                continue
+            m = cstore.read_manifest(mid)
+            if m.kind == INCREMENTAL and m.base_id == base.checkpoint_id:
+                history.record(m.payload_bytes / base.payload_bytes)
+    return RestoredRun(model=model, tracker=out.tracker, history=history,
+                       baseline_id=base.checkpoint_id,
+                       baseline_payload_bytes=base.payload_bytes, manifest=target,
+                       chain_ids=[m.checkpoint_id for m in chain])
+
+
+def _restore_errors():
+    """(IntegrityError, FormatError) of this package and, when the caller's
+    store raises the reference package's own classes, of that package too."""
+    from . import errors
+    out = [errors.IntegrityError, errors.FormatError]
+    import sys
+    ref = sys.modules.get("deltasnap.errors")
+    if ref is not None:
+        out += [ref.IntegrityError, ref.FormatError]
+    return tuple(out)
+
+
 def restore(cstore, *, fallback: bool = False, checkpoint_id: int | None = None,
-            device=None, verify_on_device: bool = False) -> RestoredTables:
-    """restore() over a reference-compatible CheckpointStore (engine.py:515-535).
+            device=None, verify_on_device: bool = False,
+            row_range: tuple | None = None) -> RestoredRun:
+    """Rebuild the model from the newest valid checkpoint (engine.py:515-535).
 
-    Chain resolution is the store's (host); decoding and scattering run on
-    the GPU.  verify_on_device: the shard payloads' CRC32 checks of
-    store.verify (store.py:488-507) run on the device after the H2D copy
-    (stage_chain) instead of on the host.
+    cstore: the reference's CheckpointStore (or anything with its
+    resolve_chain / verify_chain / valid_ids / read_manifest / store.get).
+    Chain resolution stays on the host; decode and scatter run on the GPU.
+    verify_on_device: the shard payloads' CRC32 checks of store.verify run on
+    the device after the H2D copy (stage_chain); presence, sizes and the dense
+    objects' CRC32 are checked on the host.  row_range=(lo, hi): restore only
+    that global row range of every table (one rank of a row-sharded restore).
+    With fallback=True a checkpoint failing integrity checks is skipped and
+    the next older one tried.
     """
-    def restore_at(cid):
-        if verify_on_device:
-            # presence and sizes on the host, checksums on the device
-            chain = cstore.resolve_chain(cid)
-            for m in chain:
-                for e in list(m.shards.values()) + [m.dense]:
-                    try:
-                        n = len(cstore.store.get(e.key))
-                    except KeyError:
-                        raise IntegrityError(f"missing object {e.key!r}") from None
-                    if n != e.nbytes:
-                        raise IntegrityError(f"size mismatch for {e.key!r}: {n} != {e.nbytes}")
-        else:
-            chain = cstore.verify_chain(cid)
-        target = chain[-1]
-        shapes = {tid: (info.rows, info.dim) for tid, info in target.tables.items()}
-        plan = [(m.kind, [cstore.store.get(e.key) for _, e in sorted(m.shards.items())])
-                for m in chain]
-        if verify_on_device:
-            sums = [[e.crc32 for _, e in sorted(m.shards.items())] for m in chain]
-            plan = stage_chain(plan, sums, device=device)
-        out = restore_chain(plan, shapes, aux=bool(target.aux), device=device)
-        out.chain_ids = [m.checkpoint_id for m in chain]
-        out.manifest = target
-        out.dense = np.frombuffer(cstore.store.get(target.dense.key), dtype="<f4").astype(
-            np.float32)
-        return out
-
+    kw = dict(device=device, verify_on_device=verify_on_device, row_range=row_range)
     if checkpoint_id is not None:
-        return restore_at(checkpoint_id)
+        return _restore_at(cstore, checkpoint_id, **kw)
     ids = cstore.valid_ids()
     if not ids:
         raise IntegrityError("no valid checkpoint to restore from")
+    caught = _restore_errors()
     last = None
     for cid in reversed(ids):
         try:
-            return restore_at(cid)
-        except Exception as exc:  # ours or the store's own IntegrityError/FormatError
-            if type(exc).__name__ not in ("IntegrityError", "FormatError") or not fallback:
+            return _restore_at(cstore, cid, **kw)
+        except caught as exc:
+            if not fallback:
                 raise
             last = exc
     raise IntegrityError(f"no restorable checkpoint: {last}")

@@ -9,7 +9,7 @@ transfers overlap the kernels (the paper's "background" write, engine.py:
     pipe = CheckpointPipeline(checkpointer, idx_capacity)
     for host_idx in interval_lookups:          # pinned host tensors
         pipe.submit(host_idx, seg_off, seg_tables)
-    payloads = pipe.drain()                    # [(bytes view, nbytes), ...]
+    payloads = pipe.drain()                    # [bytes, ...] with keep_outputs=True
 """
 
 from __future__ import annotations
@@ -43,7 +43,8 @@ class CheckpointPipeline:
         self.k = 0
         self.pending = None  # (slot) whose D2H is not issued yet
         self.keep = keep_outputs
-        self.outputs = []
+        self.outputs = []     # keep_outputs: every finished checkpoint's payload bytes
+        self._retained = []   # (slot, nbytes) whose D2H is issued but not copied out yet
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
@@ -51,13 +52,16 @@ class CheckpointPipeline:
         self.ev_done[slot].synchronize()        # its counts are on the host now
         _lib.raise_flags(int(self.flags_host[slot]), "checkpoint")
         n = int(self.nbytes_host[slot])
+        # this D2H rewrites host_out[slot]: copy a retained payload of the
+        # slot's previous step out first
+        self._collect(slot)
         with torch.cuda.stream(self.d2h):
             self.d2h.wait_event(self.ev_done[slot])
             self.host_out[slot][:n].copy_(self.payload[slot][:n], non_blocking=True)
             self.ev_out[slot].record(self.d2h)
         self.d2h_bytes += n
         if self.keep:
-            self.outputs.append((slot, n))
+            self._retained.append((slot, n))
 
     def submit(self, host_idx, seg_off=None, seg_tables=None) -> None:
         """Queue one checkpoint interval whose lookups are in pinned host
@@ -95,11 +99,27 @@ class CheckpointPipeline:
         self.pending = s
         self.k += 1
 
+    def _collect(self, slot: int | None = None) -> None:
+        """Copy retained payloads out of their pinned slots (all, or those of
+        `slot`) once their D2H has completed, oldest first."""
+        keep = []
+        for s, n in self._retained:
+            if slot is None or s == slot:
+                self.ev_out[s].synchronize()
+                self.outputs.append(bytes(self.host_out[s][:n].numpy()))
+            else:
+                keep.append((s, n))
+        self._retained = keep
+
     def drain(self):
-        """Issue the last D2H and wait for every transfer."""
+        """Issue the last D2H and wait for every transfer.  Returns every
+        retained payload (keep_outputs=True) as bytes, in submission order,
+        and clears the list."""
         if self.pending is not None:
             self._issue_d2h(self.pending)
             self.pending = None
         self.d2h.synchronize()
         self.compute.synchronize()
-        return [(self.host_out[s], n) for s, n in self.outputs]
+        self._collect()
+        out, self.outputs = self.outputs, []
+        return out

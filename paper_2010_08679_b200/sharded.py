@@ -90,7 +90,10 @@ class PeerCounts:
         return self._x
 
     def check(self) -> None:
-        _lib.raise_flags(int(self.flags.item()), "count exchange")
+        fl = int(self.flags.item())
+        if fl:
+            self.flags.zero_()  # a later healthy exchange must not re-raise this one
+        _lib.raise_flags(fl, "count exchange")
 
     def close(self) -> None:
         """Unmap the peers' buffers and free this rank's (every rank must be

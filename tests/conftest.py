@@ -20,6 +20,30 @@ def have_reference() -> bool:
     return os.path.isdir(os.path.join(REFERENCE_SRC, "deltasnap"))
 
 
+REFERENCE_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_path():
+    """Where the unmodified reference package can be imported from: the
+    offline pip install under baseline/_ref (travels to the GPU box), else the
+    read-only source tree (build container only); None if neither exists."""
+    for p in (REFERENCE_INSTALL, REFERENCE_SRC):
+        if os.path.isdir(os.path.join(p, "deltasnap")):
+            return p
+    return None
+
+
+def import_reference_anywhere():
+    p = reference_path()
+    if p is None:
+        pytest.skip("the reference package is not installed (baseline/_ref)")
+    sys.dont_write_bytecode = True
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    import deltasnap
+    return deltasnap
+
+
 def import_reference():
     """Import the reference package read-only (build container only)."""
     sys.dont_write_bytecode = True

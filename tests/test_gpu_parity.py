@@ -209,6 +209,83 @@ def test_bitmap_semantics(ds):
     assert tr.nbytes() == 4 * 1000
 
 
+def test_merge_in_and_scope_resets(ds, O):
+    """merge_in (tracker.py:46-49), reset_interval / reset_baseline
+    (tracker.py:120-130) and mark_baseline (:132-134) against set semantics,
+    and capture_device/capture_into with fold=1 (reset_interval) and fold=2
+    (reset_baseline) in the same pass (engine.py:278-280)."""
+    a, b = ds.DirtyBitmap(4, 100_000), ds.DirtyBitmap(4, 100_000)
+    a.mark([1, 5, 99_999])
+    b.mark([5, 6, 70_000])
+    a.merge_in(b)
+    assert a.dirty_rows()[0].tolist() == [1, 5, 6, 70_000, 99_999]
+    assert b.dirty_rows()[0].tolist() == [5, 6, 70_000]  # the argument is untouched
+    with pytest.raises(ds.ShapeError):
+        a.merge_in(ds.DirtyBitmap(4, 99_999))
+    with pytest.raises(ds.ShapeError):
+        a.merge_in(ds.DirtyBitmap(5, 100_000))
+
+    rng = np.random.default_rng(5)
+    rows = {0: 1_000_003, 1: 70_001, 2: 17}
+    for path in ("host", "capture_device", "capture_into"):
+        tr = ds.ModelTracker(rows)
+        ref_i = {t: set() for t in rows}
+        ref_b = {t: set() for t in rows}
+        for phase, fold in enumerate((1, 1, 2, 1, 2, 0)):
+            for t, r in rows.items():
+                idx = rng.integers(0, r, size=min(3 * r, 50_000))
+                tr.mark(t, idx)
+                ref_i[t] |= set(idx.tolist())
+            if phase == 3:  # restore-time rebuild of the baseline scope
+                extra = {t: rng.integers(0, r, 100) for t, r in rows.items()}
+                for t in rows:
+                    tr.mark_baseline(t, extra[t])
+                    ref_b[t] |= set(extra[t].tolist())
+            want_i = {t: np.array(sorted(ref_i[t]), np.int64) for t in rows}
+            want_u = {t: np.array(sorted(ref_i[t] | ref_b[t]), np.int64) for t in rows}
+            if path == "host":
+                view = tr.capture()
+                got_i, got_u = view.interval_rows, view.baseline_rows
+                if fold == 1:
+                    tr.reset_interval()
+                elif fold == 2:
+                    tr.reset_baseline()
+            elif path == "capture_device":
+                iv, uv = tr.capture_device(fold=fold)
+                got_i = {t: iv[t].cpu().numpy() for t in rows}
+                got_u = {t: uv[t].cpu().numpy() for t in rows}
+            else:
+                total = sum(rows.values())
+                ids_i = torch.empty(total, dtype=torch.int64, device="cuda")
+                ids_u = torch.empty(total, dtype=torch.int64, device="cuda")
+                ci = torch.zeros(len(rows) + 1, dtype=torch.int64, device="cuda")
+                cu = torch.zeros(len(rows) + 1, dtype=torch.int64, device="cuda")
+                tr.capture_into(ids_u, cu, fold=0, scope="baseline")
+                tr.capture_into(ids_i, ci, fold=fold, scope="interval")
+                ci, cu = ci.cpu().numpy(), cu.cpu().numpy()
+                assert ci[-1] == ci[:-1].sum() and cu[-1] == cu[:-1].sum()
+                oi = np.concatenate([[0], np.cumsum(ci[:-1])])
+                ou = np.concatenate([[0], np.cumsum(cu[:-1])])
+                hi, hu = ids_i.cpu().numpy(), ids_u.cpu().numpy()
+                got_i = {t: hi[oi[k]:oi[k] + ci[k]] for k, t in enumerate(rows)}
+                got_u = {t: hu[ou[k]:ou[k] + cu[k]] for k, t in enumerate(rows)}
+            for t in rows:
+                assert np.array_equal(got_i[t], want_i[t]), (path, phase, t)
+                assert np.array_equal(got_u[t], want_u[t]), (path, phase, t)
+            if fold == 1:
+                for t in rows:
+                    ref_b[t] |= ref_i[t]
+                    ref_i[t] = set()
+            elif fold == 2:
+                for t in rows:
+                    ref_b[t], ref_i[t] = set(), set()
+            for t in rows:
+                assert np.array_equal(tr.interval_bitmap(t).dirty_rows()[0],
+                                      np.array(sorted(ref_i[t]), np.int64)), (path, phase)
+                assert np.array_equal(tr.baseline_bitmap(t).dirty_rows()[0],
+                                      np.array(sorted(ref_b[t]), np.int64)), (path, phase)
+
+
 def test_capture_large_vs_oracle(ds, O):
     rng = np.random.default_rng(1)
     rows = {0: 3_000_000, 1: 65_537, 2: 1, 3: 1_000_003}
@@ -650,6 +727,60 @@ def test_staged_checkpoint_matches_direct(ds, O):
     ck.checkpoint(staged_rows=1000)
     with pytest.raises(ValueError):
         ck.fetch()
+
+
+def test_staged_capacity_is_flagged_not_overread(ds):
+    """A staging buffer smaller than the dirty total (fresh checkpointer: the
+    buffer is exactly staged_rows long) raises at fetch; the writer reads no
+    row past the buffer."""
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    rng = np.random.default_rng(41)
+    rows = {0: 2_000_000}
+    tabs = [ds.DeviceTable(0, torch.randn((rows[0], 128), device="cuda"))]
+    ck = ShardedCheckpointer(tabs, 4, adaptive_overrides={4: None}, device="cuda")
+    ck.mark(ds.LookupStream.pack({0: rng.integers(0, rows[0], 200_000)}, rows).to("cuda"))
+    ck.checkpoint(staged_rows=64)
+    with pytest.raises(ValueError):
+        ck.fetch()
+    torch.cuda.synchronize()  # the context is healthy: no illegal address
+    ck.mark(ds.LookupStream.pack({0: rng.integers(0, rows[0], 1000)}, rows).to("cuda"))
+    ck.checkpoint()
+    buf, n = ck.fetch()
+    assert n == 24 + ck.rec * int(ck.counts[0].item())
+
+
+@pytest.mark.parametrize("packed", (False, True))
+def test_checkpoint_pipeline_payloads(ds, O, packed):
+    """CheckpointPipeline (the e2e path): 5 consecutive checkpoints through
+    the double-buffered H2D -> K1/K2/K3 -> D2H slots, each step's D2H'd bytes
+    equal to the oracle's payload for that step's lookups (no
+    slot aliasing with keep_outputs)."""
+    from paper_2010_08679_b200.pipeline import CheckpointPipeline
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    rng = np.random.default_rng(51)
+    rows = {0: 5000, 1: 300_000, 2: 40}
+    vals = {t: rng.standard_normal((r, 16)).astype(np.float32) for t, r in rows.items()}
+    tabs = [ds.DeviceTable(t, torch.from_numpy(vals[t]).cuda()) for t in rows]
+    ck = ShardedCheckpointer(tabs, 8, device="cuda")
+    steps = [{t: rng.integers(0, r, int(rng.integers(1, 20_000))) for t, r in rows.items()}
+             for _ in range(5)]
+    cap = max(sum(v.size for v in st.values()) for st in steps)
+    pipe = CheckpointPipeline(ck, cap * 8, torch.uint8 if packed else torch.int32,
+                              keep_outputs=True)
+    for st in steps:
+        if packed:
+            pipe.submit(ds.LookupStream.pack(st, rows))
+        else:
+            idx = torch.from_numpy(np.concatenate([st[t] for t in rows]).astype(np.int32))
+            seg = np.concatenate([[0], np.cumsum([st[t].size for t in rows])]).astype(np.int64)
+            pipe.submit(idx.pin_memory(), seg, np.array(list(rows), np.int64))
+    outs = pipe.drain()
+    assert len(outs) == len(steps)
+    for st, got in zip(steps, outs):
+        sel = {t: np.unique(st[t]) for t in rows}
+        want, _, _ = O.build_shard_payload({t: (vals[t], None) for t in rows}, "incremental", sel,
+                                           8, sorted(rows))
+        assert got == want
 
 
 def test_empty_inputs(ds, O):
