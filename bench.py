@@ -862,26 +862,48 @@ def restore_launches(h, incremental):
 
 def run_restore(args):
     """C5: restore a 1 full + 5 incremental chain through the public API
-    (engine.apply_payload, i.e. one ds_restore_payload launch per payload).
+    (engine.apply_payload: one ds_restore_payload launch per payload).
 
-    value: restored fp32 row bytes (all records of the chain x 4*dim) / device
-    time of the chain with the payloads resident in HBM; e2e: the same with
-    the payload bytes H2D-copied from pinned host memory inside the timed
-    region.  Single GPU (a row-sharded restore runs the same kernels on each
-    rank's row range).
+    One process per GPU; rank g restores rows [g*R/N, (g+1)*R/N) of every
+    table (SURVEY 8(e) "Restore"), uploading only its rows' records
+    (engine.rank_slices: a slice of the full section, a binary search over
+    the sorted row column of each incremental one).  value: restored fp32
+    row bytes of all ranks / max-over-ranks device time of the chain with the
+    rank's slices resident in HBM; e2e: the same with the slices H2D-copied
+    from pinned host memory inside the timed region.
     """
     import torch
+    import torch.distributed as dist
     import paper_2010_08679_b200 as ds
-    from paper_2010_08679_b200.engine import ShardWriter, apply_payload
-    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    from paper_2010_08679_b200.engine import ShardWriter, apply_payload, rank_slices
+    from paper_2010_08679_b200.payload import parse_headers
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer, shard_rows
     from paper_2010_08679_b200.tracker import ModelTracker
 
-    dev = torch.device("cuda", 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local_rank])
+
     w = workload_of(args)
     cards, dim = w["cards"], w["dim"]
     gen = torch.Generator(device=dev)
-    gen.manual_seed(args.seed * 7919)
+    gen.manual_seed(args.seed * 7919)  # every rank builds the same chain
     tables = [ds.DeviceTable(t, torch.rand((r, dim), generator=gen, device=dev).mul_(2).sub_(1))
               for t, r in enumerate(cards)]
     # the chain: a full checkpoint, then 5 intervals of Zipf lookups
@@ -901,21 +923,31 @@ def run_restore(args):
         for t in tables:  # the training step between checkpoints
             t.values.add_(0.01)
     host = [(kind, b.cpu().numpy().tobytes()) for kind, b in chain]
-    pinned = [torch.from_numpy(np.frombuffer(h, np.uint8).copy()).pin_memory() for _, h in host]
-    from paper_2010_08679_b200.payload import parse_headers
-    rows_restored = sum(i.rows for (kind, h) in host for i in parse_headers(h, kind != "full"))
-    out = {t.table_id: ds.DeviceTable(t.table_id, torch.zeros_like(t.values)) for t in tables}
-    tr = ModelTracker({t.table_id: t.rows for t in tables}, device=dev)
+    del chain, ck, full, buf
+    # this rank's rows of every table, and its slice of every payload
+    ranges = {t: shard_rows(r, world, rank) for t, r in enumerate(cards)}
+    out = {t: ds.DeviceTable(t, torch.zeros((hi - lo, dim), device=dev), row_base=lo,
+                             total_rows=cards[t]) for t, (lo, hi) in ranges.items()}
+    tr = ModelTracker({t: o.rows for t, o in out.items()}, device=dev)
     base = {tid: tr.baseline_bitmap(tid) for tid in out}
-    dbufs = [torch.cat([b, torch.zeros(16, dtype=torch.uint8, device=dev)]) for _, b in chain]
+    slices = []
+    for kind, h in host:
+        infos = parse_headers(h, kind != "full")
+        hs, descs = rank_slices(h, infos, kind != "full", [ranges[i.table_id] for i in infos])
+        pin = torch.from_numpy(hs).pin_memory()
+        slices.append((kind, h, pin, pin.to(dev), descs))
+    rows_restored = sum(hi - lo for lo, hi in ranges.values())  # a full section restores every row
+    rows_restored_all = sum(cards)
+    chain_records_rank = sum(d[1] for kind, _, _, _, descs in slices for d in descs
+                             if kind != "full") + rows_restored
 
     def restore_once(from_host):
         checks = []
-        for (kind, h), db, pin in zip(host, dbufs, pinned):
+        for kind, h, pin, dbuf, descs in slices:
             if from_host:
-                db[:pin.numel()].copy_(pin, non_blocking=True)
+                dbuf.copy_(pin, non_blocking=True)
             checks.append(apply_payload(h, kind != "full", out, base if kind != "full" else None,
-                                        device=dev, device_buf=db, sync=False))
+                                        device=dev, device_buf=dbuf, sync=False, slice_descs=descs))
         return checks
 
     for _ in range(max(3, args.warmup)):
@@ -925,9 +957,10 @@ def run_restore(args):
     K = args.steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     times, times_e2e = [], []
-    with ClockSampler(0) as clocks:
+    with ClockSampler(local_rank) as clocks:
         for k in range(K):
             flush.fill_(k & 0xFF)
+            barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             checks = restore_once(False)
@@ -937,6 +970,7 @@ def run_restore(args):
             for c in checks:
                 c()
         for k in range(K):
+            barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             checks = restore_once(True)
@@ -944,58 +978,72 @@ def run_restore(args):
                 c()
             torch.cuda.synchronize()
             times_e2e.append(time.perf_counter() - t0)
-    t = float(np.mean(times))
-    te = float(np.mean(times_e2e))
+    t = max_over_ranks(float(np.mean(times)))
+    te = max_over_ranks(float(np.mean(times_e2e)))
 
-    # parity: every restored row (and the rebuilt since-baseline bits) against
-    # the CPU oracle applying the same chain (engine.py:459-485)
+    # parity: every restored row of this rank (and the rebuilt since-baseline
+    # bits) against the CPU oracle applying the same chain (engine.py:459-485)
     parity = None
     if args.verify_rows > 0:
         from oracle import oracle as O
         t0 = time.perf_counter()
         split = [(kind != "full", dict(O.split_sections(h, kind != "full"))) for kind, h in host]
         rows_ok = rows_n = bits_bad = 0
-        for tb in tables:
-            tid = tb.table_id
-            want = np.zeros((tb.rows, dim), np.float32)
-            bits = np.zeros((tb.rows + 7) // 8, np.uint8)
+        for tid, (lo, hi) in ranges.items():
+            want = np.zeros((cards[tid], dim), np.float32)
+            bits = np.zeros((cards[tid] + 7) // 8, np.uint8)
             for inc, secs in split:
                 if tid in secs:
                     O.apply_section(secs[tid], inc, want, None, bits if inc else None)
             got = out[tid].values.cpu().numpy()
-            rows_ok += int(np.all(got.view(np.uint32) == want.view(np.uint32), axis=1).sum())
-            rows_n += tb.rows
-            bits_bad += int(not np.array_equal(base[tid].to_bytes(), bits))
+            rows_ok += int(np.all(got.view(np.uint32) == want[lo:hi].view(np.uint32), axis=1).sum())
+            rows_n += hi - lo
+            ref_bits = np.unpackbits(bits, bitorder="little")[:cards[tid]][lo:hi]
+            got_bits = np.unpackbits(base[tid].to_bytes(), bitorder="little")[:hi - lo]
+            bits_bad += int(not np.array_equal(ref_bits, got_bits))
         parity = {"rows_checked": rows_n, "mismatches": rows_n - rows_ok + bits_bad,
-                  "baseline_bitmaps_checked": len(tables),
-                  "checked_against": "CPU oracle applying the same chain (every row of every "
-                                     "table, bit-exact float32; since-baseline bits)",
+                  "baseline_bitmaps_checked": len(ranges),
+                  "checked_against": "CPU oracle applying the same chain (every row of this "
+                                     "rank's tables, bit-exact float32; since-baseline bits)",
                   "seconds": time.perf_counter() - t0}
-    nbytes = rows_restored * dim * 4
-    h2d = sum(p.numel() for p in pinned)
-    # roofline: the restore kernels' algorithmic bytes = chain bytes read +
-    # restored fp32 rows written
-    alg = h2d + nbytes
+        if world > 1:
+            mm = torch.tensor([parity["mismatches"], rows_n], dtype=torch.int64, device=dev)
+            dist.all_reduce(mm)
+            parity["mismatches"], parity["rows_checked"] = int(mm[0].item()), int(mm[1].item())
+    h2d = sum(p.numel() for _, _, p, _, _ in slices)
+    full_bytes = sum(len(h) for _, h in host)
+    nbytes = rows_restored_all * dim * 4  # restored rows of all ranks (full section: every row)
+    rec = [i.record_size for i in parse_headers(host[0][1], False)][0]
+    # roofline: this rank's algorithmic bytes = its slices read + its restored
+    # fp32 rows written (every record of the rank is applied once per payload)
+    alg = h2d + chain_records_rank * dim * 4
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    line = {
-        "metric": "restored GB/s of embedding rows (unpack+dequantize+scatter)", "value": nbytes / t / 1e9,
-        "unit": "GB/s", "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8->f32 via f64",
-        "data": "synthetic", "config": dict(workload_desc(w), chain_records=rows_restored,
-                                            chain_bytes=h2d,
-                                            timing="CUDA events at each chain's bounds"),
-        "roofline": {"bound": "hbm", "kernel": "ds::restore_payload_kernel (one launch per payload of the chain)",
-                     "achieved": alg / t / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": alg / t / 1e9 / peak, "traffic": None},
-        "e2e": {"value": nbytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 4 * len(host) * 26},
-        "parity": parity,
-        "clocks": clocks.summary(), "gpu_launches": K * sum(restore_launches(h, kind != "full")
-                                                         for (kind, h) in host),
-    }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        line = {
+            "metric": "restored GB/s of embedding rows (unpack+dequantize+scatter)",
+            "value": nbytes / t / 1e9, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8->f32 via f64",
+            "data": "synthetic",
+            "config": dict(workload_desc(w), chain_payload_bytes=full_bytes,
+                           rank_upload_bytes=h2d, rows_per_rank=rows_restored,
+                           parallelism=f"row-sharded x{world} (rank-local slices)",
+                           timing="CUDA events at each chain's bounds, max over ranks"),
+            "roofline": {"bound": "hbm",
+                         "kernel": "ds::restore_payload_kernel (one launch per payload of the chain)",
+                         "achieved": alg / t / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / t / 1e9 / peak, "traffic": None},
+            "e2e": {"value": nbytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": 4 * len(host) * len(cards)},
+            "parity": parity,
+            "clocks": clocks.summary(),
+            "gpu_launches": K * sum(restore_launches(h, kind != "full") for (kind, h) in host),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():

@@ -151,6 +151,46 @@ __device__ __forceinline__ float deq_exact(int q, float lo, double s) {
 }
 
 // ---------------------------------------------------------------------------
+// the err_sum term without the conversion unit.  F2F (f32<->f64) issues at
+// ~1/8 of the FP32 rate on B200 (scripts/micro/pipe_rates.cu: ~0.5 warp
+// instructions per clock per SM vs ~3.7 for FFMA and ~1.95 for DFMA), and the
+// reference error of an element (engine.py:171-173: f64(x) - f64(deq32))
+// needs four of them.  Here the same value comes from integer bit arithmetic
+// and half-rate f64 ops only.
+// ---------------------------------------------------------------------------
+// f32 -> f64 by bit arithmetic: exact for normal x; +-0 and subnormals land
+// within 2^-126 of their value (rows whose range makes that matter take the
+// exact path, RowQ mode 2)
+__device__ __forceinline__ double f2d_bits(float x) {
+    const uint32_t b = __float_as_uint(x);
+    const uint32_t hi = (((b >> 3) & 0x0FFFFFFFu) + 0x38000000u) | (b & 0x80000000u);
+    return __hiloint2double((int)hi, (int)(b << 29));
+}
+// RN-even to float precision of a double in the f32 normal range, kept as a
+// double: add (half an f32 ulp - 1 + kept lsb) to the 64-bit pattern, truncate
+__device__ __forceinline__ double round_f32_in_f64(double w) {
+    uint32_t lo = (uint32_t)__double2loint(w), hi = (uint32_t)__double2hiint(w);
+    const uint32_t add = 0x0FFFFFFFu + ((lo >> 29) & 1u);
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(lo), "+r"(hi) : "r"(add));
+    return __hiloint2double((int)hi, (int)(lo & 0xE0000000u));
+}
+// a code (0..255) as a double, exactly, through the 2^52 magic (one DADD)
+__device__ __forceinline__ double code_to_f64(uint32_t q) {
+    return __dsub_rn(__hiloint2double(0x43300000, (int)q), 4503599627370496.0);
+}
+// x - deq(q) of the reference, as a double: deq(q) = f32(RN(RN(s*q) + lo))
+// (quant.py:114-115, two rounded ops), x and deq exact in f64
+__device__ __forceinline__ double err_fast(float x, uint32_t q, double s, double lod) {
+    const double w = __dadd_rn(__dmul_rn(s, code_to_f64(q)), lod);
+    return __dsub_rn(f2d_bits(x), round_f32_in_f64(w));
+}
+// a row's L2 error from its f64 sum of squares; sums below 2^-200 (only the
+// +-2^-127 stand-ins of exact zeros, or errors < 2^-100) count as 0
+__device__ __forceinline__ double row_err(double sse) {
+    return sse > 0x1p-200 ? sse * rsqrt(sse) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
 // final codes of a row with fixed (lo, hi): fp32 guard band + exact fallback
 // ---------------------------------------------------------------------------
 struct RowQ {
@@ -182,7 +222,9 @@ __device__ __forceinline__ RowQ make_rowq(float lo, float hi, int L, double y = 
     r.eps = 0.f;
     if (!(r.s > 0.0)) {
         r.mode = 1;  // scale 0 -> safe 1 -> v = 0 -> code 0 (quant.py:101-106)
-    } else if (!(rng >= 1e-30f && rng <= 1e30f && fabsf(lo) <= 1e30f && fabsf(hi) <= 1e30f)) {
+    } else if (!(rng >= 1e-21f && rng <= 1e30f && fabsf(lo) <= 1e30f && fabsf(hi) <= 1e30f)) {
+        // (range >= 1e-21: also keeps err_fast's +-0 / subnormal stand-ins
+        // below 1e-14 of the row's error)
         r.mode = 2;
     } else {
         r.mode = 0;

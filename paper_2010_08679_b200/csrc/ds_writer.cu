@@ -249,7 +249,25 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
     int tr;
     int threads = WT;
     size_t smem;
-    if (mode != 2 || !DS_GREEDY_CTA) {
+    // wide rows at 2/4/8 bits with naive ranges: one row per lane group
+    // (ds_writer_row.cuh); DS_ROW_G=0 keeps the warp-pipelined writer
+    // (A/B r02, T shard: 7.07 ms at G = 4 vs 6.95 ms for the warp-pipelined
+    // writer with fused packing: off by default, DS_ROW_G=4 selects it)
+    static const int row_g = (int)host::env_int("DS_ROW_G", 0);
+    bool row_kernel = false;
+    if (mode == 1 && c.VEC == 4 && vec4 && !p->aux && a.rec % 8 == 0 && row_g > 0 &&
+        (bw == 8 || bw == 4 || bw == 2)) {
+        writer_fn rf = select_writer_row(d, row_g, bw);
+        if (rf) {
+            fn = rf;
+            row_kernel = true;
+        }
+    }
+    if (row_kernel) {
+        tr = 32 / row_g;
+        threads = 32;
+        smem = row_writer_smem_bytes(d, row_g, a.rec);
+    } else if (mode != 2 || !DS_GREEDY_CTA) {
         // warp pipeline: tiles of 32 records, per-warp record stage + codes
         // scratch + a ring of NS row chunks of 32/G rows (+ the greedy exact
         // scratch; writer_warp_kernel computes the same layout)
@@ -272,7 +290,8 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         // incremental counts live on the device; bound by table rows
         max_tiles += (tables_host[t].rows + tr - 1) / tr;
     }
-    if (mode != 2 || !DS_GREEDY_CTA) max_tiles = (max_tiles + threads / 32 - 1) / (threads / 32);  // warps -> CTAs
+    if (!row_kernel && (mode != 2 || !DS_GREEDY_CTA))
+        max_tiles = (max_tiles + threads / 32 - 1) / (threads / 32);  // warps -> CTAs
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return host::fail(DS_ERR_CUDA, cudaGetErrorString(e));
     int per_sm = 0;

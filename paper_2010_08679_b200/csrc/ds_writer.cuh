@@ -18,6 +18,13 @@
 #include "ds_common.cuh"
 #include "ds_host.h"
 
+#ifndef DS_ERR_F2F
+#define DS_ERR_F2F 1  // 1: the err_sum term through the conversion unit; 0: err_fast (integer bits)
+#endif
+#ifndef DS_M1_FUSED
+#define DS_M1_FUSED 1  // naive 2/4/8-bit rows: codes packed as produced (code_row_m1)
+#endif
+
 namespace ds {
 
 constexpr int WT = 256;  // threads per writer CTA
@@ -225,6 +232,96 @@ struct WAcc {
     bool bad_data = false, bad_ids = false;
 };
 
+// MODE 1 at 8/4/2 bits with 128-bit element chunks: codes, the certified
+// tie check, the err_sum term and the packed bytes in ONE pass over the
+// registers -- a chunk's 4 codes are packed as they are produced, so no
+// per-element code array stays live (register pressure is the limit of
+// this kernel: 128 per thread at two CTAs per SM).
+template <int G, int C, bool PAD, bool CONTIG, int N>
+__device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x)[C * 4], bool valid,
+                                            bool row_ok, const RowQ &rq, uint8_t *rec, int lig,
+                                            int d, WAcc &acc, bool al8) {
+    using Lay = Layout<G, C, 4>;
+    constexpr int EPL = C * 4;
+    auto el = [&](int k) -> int { return CONTIG ? EPL * lig + k : Lay::elem(lig, k); };
+    const double lod = (double)rq.lo;
+    float dev = 0.f;
+    double sse = 0.0;
+    uint32_t w[C];  // chunk c's 4 codes, N bits each, LSB first (quant.py:376-382)
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        uint32_t pk = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int k = 4 * c + j;
+            // min/max ranges hold every element: no clip, v in [0, L(1+5u)];
+            // round half to even through the 1.5*2^23 magic (low mantissa
+            // bits = the code); |v - q| near 1/2 -> the exact fixup (RowQ)
+            const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
+            const float qm = __fadd_rn(v, 12582912.0f);
+            const uint32_t qi = __float_as_uint(qm) & 0x3fffffu;
+            dev = fmaxf(dev, fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))));
+            const bool in = !PAD || el(k) < d;
+#if DS_ERR_F2F
+            const double er = __dsub_rn((double)x[k],
+                                        (double)__double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)__uint_as_float(
+                                            __float_as_uint(__fsub_rn(qm, 12582912.0f)))), lod)));
+#else
+            const double er = err_fast(x[k], qi, rq.s, lod);  // engine.py:171-173
+#endif
+            if (in) sse = fma(er, er, sse);
+            pk |= (in ? qi : 0u) << (N * j);
+        }
+        w[c] = row_ok ? pk : 0u;
+    }
+    dev = grp_max<G>(dev);  // every lane shuffles (no short-circuit)
+    const bool fix = row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps);
+    if (rq.mode == 2 || !row_ok) sse = 0.0;  // mode 2: the fixup adds the exact error
+    sse = grp_sumd<G>(sse);
+    if (row_ok && lig == 0) {
+        acc.err += DS_ERR_F2F ? (sse > 0.0 ? sse * rsqrt(sse) : 0.0) : row_err(sse);
+        acc.n_rows++;
+        if (al8)
+            *reinterpret_cast<uint2 *>(rec + a.par_off) = make_uint2(__float_as_uint(rq.lo), __float_as_uint(rq.hi));
+        else
+            st_bytes_slow(rec + a.par_off, ((uint64_t)__float_as_uint(rq.hi) << 32) | __float_as_uint(rq.lo), 8);
+    }
+    if (!valid) return fix;
+    uint8_t *pk = rec + a.code_off;
+    if (CONTIG && !PAD && C == 4 && al8) {
+        // the lane's 16 contiguous codes -> one 16 / 8 / 4-byte store
+        if (N == 8) {
+            if ((a.code_off & 15) == 0 && (a.rec & 15) == 0)
+                *reinterpret_cast<uint4 *>(pk + 16 * lig) = make_uint4(w[0], w[1], w[2], w[3]);
+            else {
+                *reinterpret_cast<uint2 *>(pk + 16 * lig) = make_uint2(w[0], w[1]);
+                *reinterpret_cast<uint2 *>(pk + 16 * lig + 8) = make_uint2(w[2], w[3]);
+            }
+        } else if (N == 4) {
+            *reinterpret_cast<uint2 *>(pk + 8 * lig) = make_uint2(w[0] | (w[1] << 16), w[2] | (w[3] << 16));
+        } else {
+            *reinterpret_cast<uint32_t *>(pk + 4 * lig) = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
+        }
+        return fix;
+    }
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+        const int m = CONTIG ? C * lig + c : lig + c * G;  // chunk: elements 4m..4m+3
+        if (4 * m < d) {
+            if (N == 8) {
+                if (al8) *reinterpret_cast<uint32_t *>(pk + 4 * m) = w[c];
+                else st_bytes_slow(pk + 4 * m, w[c], 4);
+            } else if (N == 4) {
+                if (al8) *reinterpret_cast<uint16_t *>(pk + 2 * m) = (uint16_t)w[c];
+                else st_bytes_slow(pk + 2 * m, w[c], 2);
+            } else {
+                pk[m] = (uint8_t)w[c];
+            }
+        }
+    }
+    return fix;
+}
+
 // Code one row held by the G lanes of a group into its record in `rec`
 // (wire layout of payload.py:84-104): [u64 row] [f32 lo, f32 hi, codes] |
 // [dim f32] [dim f32 aux].  `cs` is the group's dim-byte code scratch,
@@ -284,6 +381,20 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
             greedy_row<G, C, VEC, PAD>(x, d, lig, row_ok, lo, hi, L, a.bins, a.steps, buf, lo, hi,
                                        acc.n_exact_dec, acc.n_exact_codes);
         const RowQ rq = make_rowq(lo, hi, L, a.invL);
+        bool fused = false;
+        if constexpr (MODE == 1 && VEC == 4 && DS_M1_FUSED && G > 1) {  // one-lane rows: measured slower
+            if (a.bitwidth == 8) {
+                fix = code_row_m1<G, C, PAD, CONTIG, 8>(a, x, valid, row_ok, rq, rec, lig, d, acc, al8);
+                fused = true;
+            } else if (a.bitwidth == 4) {
+                fix = code_row_m1<G, C, PAD, CONTIG, 4>(a, x, valid, row_ok, rq, rec, lig, d, acc, al8);
+                fused = true;
+            } else if (a.bitwidth == 2) {
+                fix = code_row_m1<G, C, PAD, CONTIG, 2>(a, x, valid, row_ok, rq, rec, lig, d, acc, al8);
+                fused = true;
+            }
+        }
+        if (!fused) {
         int q[EPL];
         double sse = 0.0;
         if (MODE == 1) {
@@ -295,6 +406,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
             // the fixup pass (fix_tile), which re-codes it in exact f64: no f64 code
             // path here, so the hot loop keeps its registers.
             float dev = 0.f;
+            const double lod = (double)lo;
 #pragma unroll
             for (int k = 0; k < EPL; k++) {
                 const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
@@ -303,19 +415,30 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
                 const float qf = __fsub_rn(qm, 12582912.0f);
                 dev = fmaxf(dev, fabsf(__fsub_rn(v, qf)));
                 // err_sum term (engine.py:171-173): exact dequantized value
-                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf), (double)lo));
+#if DS_ERR_F2F
+                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf), lod));
                 const double er = __dsub_rn((double)x[k], (double)dq);
+#else
+                const double er = err_fast(x[k], (uint32_t)q[k], rq.s, lod);
+#endif
                 if (!PAD || el(k) < d) sse = fma(er, er, sse);
             }
             dev = grp_max<G>(dev);  // every lane shuffles (no short-circuit)
             fix = row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps);
             if (rq.mode == 2) sse = 0.0;  // fix_tile adds this row's exact error
         } else {
+            const double lod = (double)lo;
+            const bool exact_err = DS_ERR_F2F || rq.mode == 2;  // err_fast's range (RowQ)
 #pragma unroll
             for (int k = 0; k < EPL; k++) {
                 q[k] = code_of(x[k], rq, acc.n_exact_codes);
-                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)q[k]), (double)lo));
-                const double er = __dsub_rn((double)x[k], (double)dq);
+                double er;
+                if (exact_err) {
+                    const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)q[k]), lod));
+                    er = __dsub_rn((double)x[k], (double)dq);
+                } else {
+                    er = err_fast(x[k], (uint32_t)q[k], rq.s, lod);
+                }
                 if (!PAD || el(k) < d) sse = fma(er, er, sse);
             }
         }
@@ -327,7 +450,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
         if (row_ok && lig == 0) {
             // row L2 norm: sqrt as sse * rsqrt(sse) (within an ulp; err_sum is a
             // diagnostic sum whose low bits depend on summation order anyway)
-            acc.err += sse > 0.0 ? sse * rsqrt(sse) : 0.0;
+            acc.err += DS_ERR_F2F ? (sse > 0.0 ? sse * rsqrt(sse) : 0.0) : row_err(sse);
             acc.n_rows++;
             if (al8)
                 *reinterpret_cast<uint2 *>(rec + a.par_off) = make_uint2(__float_as_uint(lo), __float_as_uint(hi));
@@ -420,6 +543,7 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
             }
             __syncwarp();
         }
+        }  // !fused
     }
     if (a.aux && valid) {
         float xa[EPL];
@@ -620,7 +744,11 @@ __device__ __forceinline__ void fix_rows_inline(const WriterArgs &a, const float
         for (int k = 0; k < EPL; k++) {
             const int e = el(k);
             if (row_changed && e < d) {
+#if DS_ERR_F2F
                 const double ef = __dsub_rn((double)x[k], (double)deq_exact(qfast[k], lo, rq.s));
+#else
+                const double ef = err_fast(x[k], (uint32_t)qfast[k], rq.s, (double)lo);  // as the hot loop
+#endif
                 const double ee = __dsub_rn((double)x[k], (double)deq_exact(qex[k], lo, rq.s));
                 sf = fma(ef, ef, sf);
                 se = fma(ee, ee, se);
@@ -631,7 +759,7 @@ __device__ __forceinline__ void fix_rows_inline(const WriterArgs &a, const float
         se = grp_sumd<G>(se);
         if (row_changed && lig == 0)
             acc.err += (se > 0.0 ? se * rsqrt(se) : 0.0) -
-                       (rq.mode == 2 || !(sf > 0.0) ? 0.0 : sf * rsqrt(sf));
+                       (rq.mode == 2 ? 0.0 : (DS_ERR_F2F ? (sf > 0.0 ? sf * rsqrt(sf) : 0.0) : row_err(sf)));
         __syncwarp();
         if (row_changed) {  // rewrite the record's packed codes (LSB-first bitstream)
             uint8_t *pk = rec + a.code_off;
@@ -726,7 +854,11 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
         for (int k = 0; k < EPL; k++) {
             const int e = Lay::elem(lig, k);
             if (row_changed && e < d) {
+#if DS_ERR_F2F
                 const double ef = __dsub_rn((double)x[k], (double)deq_exact(qfast[k], lo, rq.s));
+#else
+                const double ef = err_fast(x[k], (uint32_t)qfast[k], rq.s, (double)lo);  // as the hot loop
+#endif
                 const double ee = __dsub_rn((double)x[k], (double)deq_exact(qex[k], lo, rq.s));
                 sf = fma(ef, ef, sf);
                 se = fma(ee, ee, se);
@@ -737,7 +869,7 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
         se = grp_sumd<G>(se);
         if (row_changed && lig == 0)
             acc.err += (se > 0.0 ? se * rsqrt(se) : 0.0) -
-                       (rq.mode == 2 || !(sf > 0.0) ? 0.0 : sf * rsqrt(sf));
+                       (rq.mode == 2 ? 0.0 : (DS_ERR_F2F ? (sf > 0.0 ? sf * rsqrt(sf) : 0.0) : row_err(sf)));
         __syncwarp();
         if (row_changed) {  // overwrite the record's packed codes (LSB-first bitstream)
             uint8_t *pk = a.payload + s_sec[t] + (a.write_headers ? DS_HEADER_SIZE : 0) +
@@ -780,6 +912,7 @@ __device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
 #ifndef DS_WRITER_MINB
 #define DS_WRITER_MINB 2
 #endif
+
 #ifndef DS_FIX_INLINE
 #define DS_FIX_INLINE 1  // 0: flagged rows always re-coded in a pass after the warp's tiles
 #endif
@@ -1146,5 +1279,8 @@ static writer_fn select_writer(const Cfg &c) {
 writer_fn select_writer_mode0(const Cfg &c, bool pad);
 writer_fn select_writer_mode1(const Cfg &c, bool pad);
 writer_fn select_writer_mode2(const Cfg &c, bool pad);
+// one row per lane group (ds_writer_row.cu): d in {64, 128, 256}, naive 2/4/8-bit
+writer_fn select_writer_row(int d, int g, int n);
+size_t row_writer_smem_bytes(int d, int g, int64_t rec);
 
 }  // namespace ds

@@ -278,8 +278,55 @@ def _upload_payload(data, dev) -> torch.Tensor:
     return out
 
 
+_DUMMY = {}
+
+
+def _dummy_rows(dev) -> torch.Tensor:
+    if dev not in _DUMMY:
+        _DUMMY[dev] = torch.zeros(4, dtype=torch.float32, device=dev)
+    return _DUMMY[dev]
+
+
+def rank_slices(data, infos: list, incremental: bool, ranges: list):
+    """The records of each section that fall in one rank's row range
+    (SURVEY 8(e) "Restore": a slice for full sections, a binary search over
+    the sorted u64 row column for incremental ones, engine.py:459-485).
+
+    ranges: [(row_lo, row_hi)] per section.  Returns (host uint8 array of the
+    concatenated slices + 16 bytes of slack, [(body_off, nrec)] per section)
+    for ds_restore_payload against that array: a full section's body_off is
+    biased by -row_lo records, so record i still addresses global row i.  A
+    section whose row column is not strictly ascending or holds an id
+    outside the table goes whole (the kernel then flags it exactly as the
+    reference would fail it)."""
+    buf = np.frombuffer(data, dtype=np.uint8)
+    parts, descs, pos = [], [], 0
+    for info, (lo, hi) in zip(infos, ranges):
+        rec = info.record_size
+        body = buf[info.body_offset: info.body_offset + info.rows * rec]
+        if incremental:
+            k0, k1 = 0, info.rows
+            if info.rows:
+                ids = body.reshape(info.rows, rec)[:, :8].copy().view("<i8").reshape(-1)
+                ok = ids[0] >= 0 and bool(np.all(ids[1:] > ids[:-1]))
+                if ok:
+                    k0, k1 = (int(v) for v in np.searchsorted(ids, [lo, hi]))
+            parts.append(body[k0 * rec: k1 * rec])
+            descs.append((pos, k1 - k0))
+            pos += (k1 - k0) * rec
+        else:
+            k0, k1 = max(0, min(lo, info.rows)), max(0, min(hi, info.rows))
+            k1 = max(k0, k1)
+            parts.append(body[k0 * rec: k1 * rec])
+            descs.append((pos - k0 * rec, info.rows))
+            pos += (k1 - k0) * rec
+    parts.append(np.zeros(16, np.uint8))
+    return np.concatenate(parts), descs
+
+
 def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None = None,
-                  device=None, device_buf: torch.Tensor | None = None, sync: bool = True):
+                  device=None, device_buf: torch.Tensor | None = None, sync: bool = True,
+                  rank_local: bool | None = None, slice_descs: list | None = None):
     """Apply one shard payload to device tables (the loop body of
     engine.py:625-649).
 
@@ -290,14 +337,16 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
     wins; within a section FormatError precedes IntegrityError.
     device_buf: the same bytes already in device memory (no upload);
     sync=False: launch only and return a callable that checks the flags later
-    (restore pipelines check once per chain).
+    (restore pipelines check once per chain).  rank_local (default: the
+    tables are row shards and the bytes are on the host): upload only the
+    records of this rank's rows (rank_slices) instead of the whole payload.
+    slice_descs: device_buf holds rank_slices' array, these its descriptors.
     """
     dev = device_of(device)
     infos = parse_headers(data, incremental)  # FormatError for any bad header
     if not infos:
         return (lambda: None) if not sync else None
     L = _lib.lib()
-    buf = device_buf if device_buf is not None else _upload_payload(data, dev)
     flags = torch.zeros(len(infos), dtype=torch.int32, device=dev)
     # host-side checks first: sections from the first failing one on are not applied
     host_err = None
@@ -314,6 +363,28 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
         if host_err is not None:
             break
     napply = len(infos) if host_err is None else host_err[0]
+    buf = device_buf
+    body_off = [info.body_offset for info in infos]
+    nrec = [info.rows for info in infos]
+    if slice_descs is not None:
+        for k, (o, n) in enumerate(slice_descs[:napply]):
+            body_off[k], nrec[k] = o, n
+        rank_local = False
+    if rank_local is None:
+        rank_local = device_buf is None and any(
+            t.row_base > 0 or t.row_base + t.rows < t.total_rows for t in tables.values())
+    if rank_local and device_buf is None and napply:
+        ranges = [(tables[i.table_id].row_base, tables[i.table_id].row_base + tables[i.table_id].rows)
+                  for i in infos[:napply]]
+        host, descs = rank_slices(data, infos[:napply], incremental, ranges)
+        buf = torch.empty(host.size, dtype=torch.uint8, device=dev)
+        buf.copy_(torch.from_numpy(host).pin_memory(), non_blocking=True)
+        for k, (o, n) in enumerate(descs):
+            body_off[k], nrec[k] = o, n
+        apply_payload.last_h2d_bytes = int(host.size)
+    elif device_buf is None:
+        buf = _upload_payload(data, dev)
+        apply_payload.last_h2d_bytes = len(data)
     stream = _lib.stream_handle()
     # one launch per run of sections sharing (dim, bitwidth, aux) -- normally
     # the whole payload (ds_restore_payload, <= 64 sections per launch)
@@ -328,9 +399,10 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
         for j, info in enumerate(infos[k0:k1]):
             t = tables[info.table_id]
             bm = baseline.get(info.table_id) if (baseline is not None and incremental) else None
-            secs[j].body_off = info.body_offset
-            secs[j].nrec = info.rows
-            secs[j].values = t.values.data_ptr()
+            secs[j].body_off = body_off[k0 + j]
+            secs[j].nrec = nrec[k0 + j]
+            # a rank may hold no rows of a table: any valid address (nothing is written)
+            secs[j].values = t.values.data_ptr() or _dummy_rows(dev).data_ptr()
             secs[j].aux_values = t.aux.data_ptr() if (info.aux and t.aux is not None) else None
             secs[j].baseline = None if bm is None else bm.words.data_ptr()
             secs[j].ld = t.values.stride(0)

@@ -123,3 +123,120 @@ class CheckpointPipeline:
         self._collect()
         out, self.outputs = self.outputs, []
         return out
+
+
+class TrainingCheckpointLoop:
+    """Checkpoints overlapped with training (north star item 4): the payload
+    of interval k is quantized, packed and copied to pinned host memory
+    while interval k+1 trains.
+
+    The reference runs its writer on a background job thread while the
+    trainer continues (engine.py:229-233, 347-411; sim.py:329-352).  Here the
+    stall is K2 + the dirty-row gather into a staging buffer on the compute
+    stream (ShardedCheckpointer.checkpoint(staged_rows=...)); K3 then runs
+    from the staged copy on a side stream, and a background thread waits for
+    it and issues the pinned D2H on a copy stream -- the training steps never
+    wait for either.  Payload slots are double-buffered; the compute stream
+    only waits for the D2H of the checkpoint two intervals back before its
+    slot is rewritten.
+
+        loop = TrainingCheckpointLoop(ck, staged_rows)
+        for interval in ...:
+            for batch in interval: train_step(...)   # marks ck.tracker
+            loop.checkpoint()                        # returns the stall's end event
+        payloads = loop.drain()                      # [bytes, ...] in order
+    """
+
+    def __init__(self, ck: ShardedCheckpointer, staged_rows: int, keep_outputs: bool = True,
+                 on_payload=None):
+        import queue
+        import threading
+        from ._device import device_of
+        self.ck = ck
+        self.staged_rows = int(staged_rows)
+        dev = device_of(ck.device)
+        self.device = dev
+        self.copy = torch.cuda.Stream(dev)
+        self.payload = [ck.payload, torch.empty_like(ck.payload)]
+        self.host = [torch.empty(ck.payload.numel(), dtype=torch.uint8, pin_memory=True)
+                     for _ in range(2)]
+        self.meta = torch.zeros((2, 2), dtype=torch.int64, pin_memory=True)  # nbytes, flags
+        self.ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        self.keep = keep_outputs
+        self.on_payload = on_payload
+        self.outputs, self.errors = [], []
+        self.k = 0
+        self.d2h_bytes = 0
+        self._free = [threading.Event(), threading.Event()]  # the slot's D2H has completed
+        for f in self._free:
+            f.set()
+        self._q = queue.Queue()
+        self._t = threading.Thread(target=self._worker, daemon=True)
+        self._t.start()
+
+    def _worker(self) -> None:
+        try:
+            torch.cuda.set_device(self.device)
+        except Exception as e:  # every checkpoint then reports it (no silent hang)
+            self.errors.append(e)
+        while True:
+            item = self._q.get()
+            if item is None:
+                return
+            s, ev = item
+            try:
+                ev.synchronize()  # K3 of this checkpoint (and its byte count) done
+                n, fl = (int(v) for v in self.meta[s])
+                _lib.raise_flags(fl, "checkpoint")
+                with torch.cuda.stream(self.copy):
+                    self.copy.wait_event(ev)
+                    self.host[s][:n].copy_(self.payload[s][:n], non_blocking=True)
+                    self.ev_d2h[s].record(self.copy)
+                self.ev_d2h[s].synchronize()
+                self.d2h_bytes += n
+                out = bytes(self.host[s][:n].numpy()) if (self.keep or self.on_payload) else None
+                if self.keep:
+                    self.outputs.append(out)
+                if self.on_payload is not None:
+                    self.on_payload(out)
+            except Exception as e:  # surfaced by drain()
+                self.errors.append(e)
+            finally:
+                self._free[s].set()
+                self._q.task_done()
+
+    def checkpoint(self):
+        """The interval ends: stall (capture + staging) on the current stream,
+        then K3 and the D2H in the background.  Returns the event marking the
+        end of the stall (training may update the tables after it)."""
+        s = self.k & 1
+        # the slot's previous payload (two checkpoints back) must have left:
+        # normally long done, the host wait is then immediate
+        self._free[s].wait()
+        self._free[s].clear()
+        self.ck.payload = self.payload[s]
+        stall_end = self.ck.checkpoint(staged_rows=self.staged_rows)
+        side = self.ck._side
+        with torch.cuda.stream(side):
+            self.meta[s, 0:1].copy_(self.ck.writer.sec_off[-1:], non_blocking=True)
+            self.meta[s, 1:2].copy_(self.ck.writer.flags.to(torch.int64), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        self._q.put((s, ev))
+        self.k += 1
+        return stall_end
+
+    def drain(self) -> list:
+        """Wait for every queued checkpoint; raise the first error; return
+        (and clear) the retained payloads in checkpoint order."""
+        self._q.join()
+        if self.errors:
+            e, self.errors = self.errors[0], []
+            raise e
+        out, self.outputs = self.outputs, []
+        return out
+
+    def close(self) -> None:
+        self.drain()
+        self._q.put(None)
+        self._t.join()

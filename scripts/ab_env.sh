@@ -1,0 +1,22 @@
+#!/bin/bash
+# A/B of environment settings (each argument: "VAR=val VAR2=val" or "" for default)
+# on bench.py workloads WLS; REPS interleaved rounds; parity checked each run.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+REPS=${REPS:-2}
+for r in $(seq $REPS); do
+  for v in "$@"; do
+    for wl in ${WLS:-T}; do
+      env $v timeout 600 python bench.py --workload $wl --no-cpu --no-e2e --steps ${STEPS:-10} --warmup 3 --verify-rows ${VROWS:-200000} ${BENCH_ARGS:-} > gpurun_out/abe.json 2> gpurun_out/abe_err.txt
+      python - "$v" "$wl" <<'PY'
+import json,sys
+v,wl=sys.argv[1],sys.argv[2]
+try:
+    d=json.loads(open("gpurun_out/abe.json").read().strip().splitlines()[-1])
+except Exception as e:
+    print(v, wl, "FAILED", e); print(open("gpurun_out/abe_err.txt").read()[-3000:]); sys.exit()
+p=d['phases']; par=d.get('parity') or {}
+print(f"{(v or 'default'):40s} {wl:10s} ms/step {d['ms_per_step']:.4f} " + ' '.join(f"{k} {x['ms']*1000:.1f}" for k,x in p.items()) + f" frac {d['roofline']['frac']:.3f} parity {par.get('records_checked')}/{par.get('mismatches')} {par.get('first_mismatch')}")
+PY
+    done
+  done
+done

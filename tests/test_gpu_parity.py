@@ -508,6 +508,60 @@ def test_restore_chain_matches_golden(ds, golden, bw):
         assert np.array_equal(u32(cat), u32(g[f"{tag}_values_t{t}"]))
 
 
+@pytest.mark.parametrize("world", (2, 4))
+def test_rank_local_restore_chain_vs_oracle(ds, O, world):
+    """Row-sharded restore of a 1 full + 3 incremental chain (C5's shape):
+    each rank uploads only its rows' records (engine.rank_slices) and its
+    tables equal the oracle's restore of the whole chain, rows and
+    since-baseline bits; the ranks' uploads add up to the record bytes."""
+    from paper_2010_08679_b200.engine import apply_payload
+    from paper_2010_08679_b200.sharded import shard_rows
+    rng = np.random.default_rng(61)
+    rows = {0: 10_000, 1: 333, 2: 70_001}
+    vals = {t: rng.standard_normal((r, 16)).astype(np.float32) for t, r in rows.items()}
+    chain = [("full", O.build_shard_payload({t: (v, None) for t, v in vals.items()}, "full", None,
+                                            8, sorted(rows))[0])]
+    for k in range(3):
+        sel = {t: np.unique(rng.integers(0, r, r // 3)) for t, r in rows.items()}
+        for t in rows:
+            vals[t] = vals[t] + np.float32(0.01)
+        chain.append(("incremental", O.build_shard_payload(
+            {t: (v, None) for t, v in vals.items()}, "incremental", sel, 8, sorted(rows))[0]))
+    want = {t: np.zeros((r, 16), np.float32) for t, r in rows.items()}
+    bits = {t: np.zeros((r + 7) // 8, np.uint8) for t, r in rows.items()}
+    for kind, blob in chain:
+        inc = kind == "incremental"
+        for tid, sec in O.split_sections(blob, inc):
+            O.apply_section(sec, inc, want[tid], None, bits[tid] if inc else None)
+    h2d = 0
+    for g in range(world):
+        lo_hi = {t: shard_rows(r, world, g) for t, r in rows.items()}
+        # every table's own rank range: restore_chain takes one range, so do it per table set
+        out = {}
+        for t, (lo, hi) in lo_hi.items():
+            part = ds.restore_chain([(k, [b]) for k, b in chain], {t2: (rows[t2], 16) for t2 in rows},
+                                    row_range=(lo, hi))
+            out[t] = part
+        for t, (lo, hi) in lo_hi.items():
+            got = out[t].tables[t].values.cpu().numpy()
+            assert np.array_equal(u32(got), u32(want[t][lo:hi])), (g, t)
+            b_ref = np.unpackbits(bits[t], bitorder="little")[:rows[t]][lo:hi]
+            b_got = np.unpackbits(out[t].tracker.baseline_bitmap(t).to_bytes(),
+                                  bitorder="little")[:hi - lo]
+            assert np.array_equal(b_got, b_ref), (g, t)
+    # upload volume of one rank's pass over the chain vs the whole payloads
+    tabs = {t: ds.DeviceTable(t, torch.zeros((rows[t] // world + 1, 16), device="cuda"),
+                              row_base=0, total_rows=rows[t]) for t in rows}
+    for t in tabs:
+        tabs[t] = ds.DeviceTable(t, torch.zeros((shard_rows(rows[t], world, 0)[1], 16), device="cuda"),
+                                 row_base=0, total_rows=rows[t])
+    for kind, blob in chain:
+        apply_payload(blob, kind == "incremental", tabs)
+        h2d += apply_payload.last_h2d_bytes
+    total = sum(len(b) for _, b in chain)
+    assert h2d < total * (1.0 / world + 0.05), (h2d, total)
+
+
 def test_restore_errors(ds, O):
     x = np.random.default_rng(0).normal(size=(4, 5)).astype(np.float32)
     blob, _, _ = O.build_section(0, x, np.array([0, 2]), bitwidth=3)
@@ -781,6 +835,48 @@ def test_checkpoint_pipeline_payloads(ds, O, packed):
         want, _, _ = O.build_shard_payload({t: (vals[t], None) for t in rows}, "incremental", sel,
                                            8, sorted(rows))
         assert got == want
+
+
+@pytest.mark.parametrize("bw", (8, 4))
+def test_checkpoints_overlapped_with_training(ds, O, bw):
+    """TrainingCheckpointLoop (north star item 4): interval k's payload is
+    written from the staged copy and copied out while interval k+1's
+    training steps (ds_train_apply, np.add.at semantics, dirty bits marked
+    on the fly) already mutate the tables; every payload still equals the
+    oracle's for the tables as they were at the end of interval k."""
+    from paper_2010_08679_b200.pipeline import TrainingCheckpointLoop
+    from paper_2010_08679_b200.sharded import ShardedCheckpointer
+    from paper_2010_08679_b200.train import apply_packed, pack_batches
+    rng = np.random.default_rng(71)
+    rows = {0: 3000, 1: 200_000, 2: 50}
+    dim = 16
+    tabs = {t: ds.DeviceTable(t, torch.from_numpy(rng.standard_normal((r, dim)).astype(np.float32)).cuda())
+            for t, r in rows.items()}
+    ck = ShardedCheckpointer([tabs[t] for t in sorted(rows)], bw, adaptive_overrides={bw: None},
+                             device="cuda")
+    loop = TrainingCheckpointLoop(ck, staged_rows=sum(rows.values()))
+    want = []
+    for k in range(4):
+        touched = {t: [] for t in rows}
+        for b in range(6):  # the interval's training steps
+            batch = {}
+            for t, r in rows.items():
+                idx = rng.integers(0, r, int(rng.integers(1, 1500)))
+                batch[t] = (idx, (rng.standard_normal((idx.size, dim)) * 0.01).astype(np.float32))
+                touched[t].append(idx)
+            apply_packed(tabs, pack_batches(tabs, [batch]), tracker=ck.tracker, sorted_runs=False)
+        stall_end = loop.checkpoint()
+        # the tables as the checkpoint saw them (test-only sync at the stall's end)
+        stall_end.synchronize()
+        snap = {t: (tabs[t].values.cpu().numpy(), None) for t in rows}
+        sel = {t: np.unique(np.concatenate(touched[t])) for t in rows}
+        want.append(O.build_shard_payload(snap, "incremental", sel, bw, sorted(rows),
+                                          adaptive={bw: (1, 0.5)})[0])
+    got = loop.drain()
+    loop.close()
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert g == w
 
 
 def test_empty_inputs(ds, O):
