@@ -291,6 +291,30 @@ DS_API int ds_train_apply_sorted(const ds_train_table *tables_host, int ntables,
                                  const int64_t *order, const float *delta, uint32_t *flags,
                                  void *stream);
 
+/* The same update for a whole interval with the in-tree stable radix sort
+ * (ds_sort_pairs_u32): idx (device int64, table t's lookups at positions
+ * [table_off[t], table_off[t+1]) of a host offset array, batch order inside
+ * a table) and delta ([n, dim]); the (table, row) pairs are stably sorted,
+ * each row's run is applied in np.add.at order by one warp and its dirty
+ * bit set.  Out-of-range ids set DS_FLAG_BOUNDS and are skipped.  Needs
+ * ceil(log2(ntables)) + ceil(log2(max_rows + 1)) <= 32 and a workspace of
+ * ds_train_interval_workspace_size(n) + ds_train_interval_delta_bytes(n, dim)
+ * bytes (the sort, then the deltas gathered into sorted order). */
+DS_API size_t ds_train_interval_workspace_size(int64_t n);
+DS_API size_t ds_train_interval_delta_bytes(int64_t n, int64_t dim);
+DS_API int ds_train_apply_interval(const ds_train_table *tables_host, int ntables,
+                                   const int64_t *table_off_host, int64_t dim, const int64_t *idx,
+                                   const float *delta, void *workspace, size_t workspace_bytes,
+                                   uint32_t *flags, void *stream);
+
+/* Stable LSD radix sort (8-bit digits) of n (u32 key, u32 value) pairs by the
+ * low key_bits bits of the key; inputs intact, outputs must not alias them;
+ * workspace of ds_sort_workspace_size(n) bytes. */
+DS_API size_t ds_sort_workspace_size(int64_t n);
+DS_API int ds_sort_pairs_u32(const uint32_t *keys_in, const uint32_t *vals_in, uint32_t *keys_out,
+                             uint32_t *vals_out, int64_t n, int key_bits, void *workspace,
+                             size_t workspace_bytes, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Payload checksum (store.py:46-47 checksum())      */
 /* ------------------------------------------------------------------ */

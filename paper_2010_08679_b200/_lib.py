@@ -141,6 +141,11 @@ _SIGNATURES = {
     "ds_restore_payload": (_I, [_P, _P, _I, _I64, _I, _I, _I, _P, _P]),
     "ds_train_apply": (_I, [_P, _I, _I, _I64, _P, _P, _P, _P, _P]),
     "ds_train_apply_sorted": (_I, [_P, _I, _P, _I64, _P, _P, _P, _P, _P]),
+    "ds_train_interval_workspace_size": (_SZ, [_I64]),
+    "ds_train_interval_delta_bytes": (_SZ, [_I64, _I64]),
+    "ds_train_apply_interval": (_I, [_P, _I, _P, _I64, _P, _P, _P, _SZ, _P, _P]),
+    "ds_sort_workspace_size": (_SZ, [_I64]),
+    "ds_sort_pairs_u32": (_I, [_P, _P, _P, _P, _I64, _I, _P, _SZ, _P]),
     "ds_crc32_workspace_size": (_SZ, [_I64]),
     "ds_crc32": (_I, [_P, _I64, _P, _P, _SZ, _P]),
     "ds_peer_buffer_size": (_SZ, [_I, _I]),

@@ -17,7 +17,7 @@ import torch
 from . import _lib
 from ._device import check_flags, new_flags, to_device
 
-MAX_IDS_PER_BATCH = 4096  # ds_train_apply's per-(table, batch) sort capacity
+MAX_IDS_PER_BATCH = 4096  # ds_train_apply's per-(table, batch) sort capacity (sorted_runs=False)
 
 
 def pack_batches(tables: dict, batches: list, device=None):
@@ -42,31 +42,30 @@ def pack_batches(tables: dict, batches: list, device=None):
     idx = torch.cat(idx_parts) if seg[-1] else torch.zeros(1, dtype=torch.int64, device=dev)
     delta = torch.cat(delta_parts) if seg[-1] else torch.zeros((1, dim), device=dev)
     seg_off = torch.tensor(seg, dtype=torch.int64, device=dev)
-    return idx, delta, seg_off, len(batches)
+    return PackedBatches((idx, delta, seg_off, len(batches)), np.asarray(seg, np.int64))
+
+
+class PackedBatches(tuple):
+    """(idx, delta, seg_off, nbatches) with the host copy of seg_off."""
+
+    def __new__(cls, items, host_seg):
+        obj = super().__new__(cls, items)
+        obj.host_seg = host_seg
+        return obj
 
 
 def apply_packed(tables: dict, packed, tracker=None, sorted_runs: bool = True) -> None:
     """pack_batches' output applied on the device (asynchronous; with a
     tracker, id errors surface at its next sync like mark_batch).
 
-    sorted_runs: one stable device sort per table of the whole interval's
-    ids, then ds_train_apply_sorted (a warp per distinct row, all its updates
-    in np.add.at order); else ds_train_apply (a CTA per table walking the
-    batches with a shared-memory sort per batch)."""
+    sorted_runs (default): the whole interval in one pass -- an in-tree
+    stable radix sort of (table, row) keys groups each row's updates in array
+    order, then a warp per run applies them (ds_train_apply_interval); else
+    ds_train_apply (a CTA per table walking the batches with a shared-memory
+    sort per batch)."""
     idx, delta, seg_off, nb = packed
     tids = sorted(tables)
     dim = tables[tids[0]].dim
-    if sorted_runs:
-        seg = seg_off.cpu().numpy()
-        toff = np.array([seg[k * nb] for k in range(len(tids))] + [seg[-1]], dtype=np.int64)
-        rows_s, order = [], []
-        for k in range(len(tids)):
-            a0, a1 = int(toff[k]), int(toff[k + 1])
-            r, perm = torch.sort(idx[a0:a1], stable=True)
-            rows_s.append(r)
-            order.append(perm + a0)
-        rows_s = torch.cat(rows_s) if toff[-1] else idx
-        order = torch.cat(order) if toff[-1] else idx
     descs = (_lib.TrainTable * len(tids))()
     for k, t in enumerate(tids):
         tb = tables[t]
@@ -76,17 +75,32 @@ def apply_packed(tables: dict, packed, tracker=None, sorted_runs: bool = True) -
         descs[k].ld = tb.values.stride(0)
         descs[k].rows = tb.rows
     flags = tracker._flags if tracker is not None else new_flags(idx.device)
+    L = _lib.lib()
     if sorted_runs:
-        _lib.check(_lib.lib().ds_train_apply_sorted(
-            ctypes.cast(descs, ctypes.c_void_p), len(tids), toff.ctypes.data_as(ctypes.c_void_p), dim,
-            rows_s.data_ptr(), order.data_ptr(), delta.data_ptr(), flags.data_ptr(),
-            _lib.stream_handle()), "train_apply_sorted")
+        seg = packed_table_offsets(packed, len(tids))
+        n = int(seg[-1])
+        nbytes = int(L.ds_train_interval_workspace_size(n)) + int(L.ds_train_interval_delta_bytes(n, dim))
+        ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device=idx.device)
+        _lib.check(L.ds_train_apply_interval(
+            ctypes.cast(descs, ctypes.c_void_p), len(tids), seg.ctypes.data_as(ctypes.c_void_p), dim,
+            idx.data_ptr(), delta.data_ptr(), ws.data_ptr(), ws.numel(), flags.data_ptr(),
+            _lib.stream_handle()), "train_apply_interval")
     else:
-        _lib.check(_lib.lib().ds_train_apply(ctypes.cast(descs, ctypes.c_void_p), len(tids), nb, dim,
-                                             idx.data_ptr(), delta.data_ptr(), seg_off.data_ptr(),
-                                             flags.data_ptr(), _lib.stream_handle()), "train_apply")
+        _lib.check(L.ds_train_apply(ctypes.cast(descs, ctypes.c_void_p), len(tids), nb, dim,
+                                    idx.data_ptr(), delta.data_ptr(), seg_off.data_ptr(),
+                                    flags.data_ptr(), _lib.stream_handle()), "train_apply")
     if tracker is None:
         check_flags(flags, "apply_batches")
+
+
+def packed_table_offsets(packed, ntables: int) -> np.ndarray:
+    """Host int64 [ntables + 1]: table t's lookups of a packed interval.
+    (pack_batches keeps the host copy; a device seg_off is read once.)"""
+    idx, delta, seg_off, nb = packed
+    seg = getattr(packed, "host_seg", None)
+    if seg is None:
+        seg = seg_off.cpu().numpy()
+    return np.array([seg[k * nb] for k in range(ntables)] + [seg[-1]], dtype=np.int64)
 
 
 def apply_batches(tables: dict, batches: list, tracker=None, device=None) -> None:

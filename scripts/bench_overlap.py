@@ -51,7 +51,7 @@ loop = TrainingCheckpointLoop(ck, staged_rows=dirty_cap)
 
 def train_interval(i0):
     for s in range(NB):
-        apply_packed(tabs, batches[(i0 + s) % POOL][1], tracker=ck.tracker, sorted_runs=False)
+        apply_packed(tabs, batches[(i0 + s) % POOL][1], tracker=ck.tracker)
 
 
 # warm-up (and a clean tracker)
@@ -107,7 +107,8 @@ loop.close()
 alone = float(np.median(t_alone))
 with_ck = float(np.median(t_train))
 print(json.dumps({
-    "what": "C2 training steps (ds_train_apply, np.add.at semantics, dirty bits on the fly) with "
+    "what": "C2 training steps (ds_train_apply_interval per batch: in-tree stable radix sort, np.add.at "
+            "semantics, dirty bits on the fly) with "
             "each interval's checkpoint (8-bit naive) running beside the next interval",
     "steps_per_interval": NB, "lookups_per_step": B * len(cards),
     "interval_train_ms_alone": alone, "interval_train_ms_with_checkpoints": with_ck,

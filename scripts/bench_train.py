@@ -54,4 +54,9 @@ print(json.dumps({"what": "C2 interval of training updates (np.add.at semantics)
                   "ms_tracked": min(res[True]),
                   "tracking_overhead_ms": min(res[True]) - min(res[False]),
                   "lookups": NB * B * len(cards), "sorted_runs": SORTED,
-                  "note": "sorted_runs includes the per-table stable torch.sort of the interval"}))
+                  "bytes_per_interval": NB * B * len(cards) * (8 + 3 * 4 * D),
+                  "GB/s": NB * B * len(cards) * (8 + 3 * 4 * D) / (min(res[True]) / 1e3) / 1e9,
+                  "note": ("sorted_runs: ds_train_apply_interval (in-tree stable radix sort of "
+                           "(table, row) keys, deltas gathered into sorted order, a warp per run, a "
+                           "CTA per hot run); bytes = per lookup 8 (id) + 3 x 4d (delta read, row "
+                           "read + write)") if SORTED else "ds_train_apply: a CTA per table, batches in order"}))

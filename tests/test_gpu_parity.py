@@ -730,6 +730,66 @@ def test_apply_batches_matches_np_add_at(ds, sorted_runs):
         assert np.array_equal(view.interval_rows[t], ref.interval_rows[t]), t
 
 
+@pytest.mark.parametrize("n,bits", [(1, 1), (2047, 8), (2049, 9), (100_000, 17), (3_000_001, 29),
+                                     (500_000, 32)])
+def test_sort_pairs_is_a_stable_sort(ds, n, bits):
+    """ds_sort_pairs_u32 (the training step's in-tree radix sort) equals
+    numpy's stable argsort on the low key bits, ties in input order."""
+    import ctypes
+    from paper_2010_08679_b200 import _lib
+    rng = np.random.default_rng(n + bits)
+    hi = 1 << bits
+    keys = rng.integers(0, min(hi, 1 << 31), n, dtype=np.int64)
+    keys[rng.random(n) < 0.3] = rng.integers(0, 4) % hi  # heavy ties
+    keys = (keys % hi).astype(np.uint32)
+    vals = np.arange(n, dtype=np.uint32)
+    L = _lib.lib()
+    k_in = torch.from_numpy(keys.view(np.int32)).cuda()
+    v_in = torch.from_numpy(vals.view(np.int32)).cuda()
+    k_out, v_out = torch.empty_like(k_in), torch.empty_like(v_in)
+    ws = torch.empty(int(L.ds_sort_workspace_size(n)), dtype=torch.uint8, device="cuda")
+    _lib.check(L.ds_sort_pairs_u32(k_in.data_ptr(), v_in.data_ptr(), k_out.data_ptr(), v_out.data_ptr(),
+                                   n, bits, ws.data_ptr(), ws.numel(), _lib.stream_handle()), "sort")
+    order = np.argsort(keys & np.uint32(hi - 1 if bits < 32 else 0xFFFFFFFF), kind="stable")
+    assert np.array_equal(v_out.cpu().numpy().view(np.uint32), vals[order])
+    assert np.array_equal(k_out.cpu().numpy().view(np.uint32), keys[order])
+    assert np.array_equal(k_in.cpu().numpy().view(np.uint32), keys)  # inputs intact
+
+
+def test_interval_training_hot_rows_and_bounds(ds):
+    """ds_train_apply_interval: a row hit 5,000 times in one interval (runs far
+    longer than the 32-occurrence prefetch), singletons, and out-of-range ids
+    (BoundsError at the tracker's next sync, never applied)."""
+    from paper_2010_08679_b200.train import apply_packed, pack_batches
+    rng = np.random.default_rng(77)
+    rows, dim = {0: 100_000, 1: 7}, 16
+    vals = {t: rng.standard_normal((r, dim)).astype(np.float32) for t, r in rows.items()}
+    tabs = {t: ds.DeviceTable(t, torch.from_numpy(vals[t].copy()).cuda()) for t in rows}
+    tr = ds.ModelTracker(rows)
+    batches = []
+    for b in range(3):
+        batch = {}
+        for t, r in rows.items():
+            idx = np.where(rng.random(2000) < 0.85, 3 % r, rng.integers(0, r, 2000)).astype(np.int64)
+            batch[t] = (idx, (rng.standard_normal((2000, dim)) * 0.01).astype(np.float32))
+        batches.append(batch)
+    apply_packed(tabs, pack_batches(tabs, batches), tracker=tr)
+    want = {t: vals[t].copy() for t in rows}
+    for batch in batches:
+        for t in sorted(batch):
+            np.add.at(want[t], batch[t][0], batch[t][1])
+    for t in rows:
+        assert np.array_equal(u32(tabs[t].values.cpu().numpy()), u32(want[t])), t
+    bad = [{0: (np.array([5, 100_000, -1, 5]), np.ones((4, dim), np.float32)), 1: batches[0][1]}]
+    apply_packed(tabs, pack_batches(tabs, bad), tracker=tr)
+    with pytest.raises(ds.BoundsError):
+        tr.capture()
+    np.add.at(want[0], np.array([5, 5]), np.ones((2, dim), np.float32))
+    np.add.at(want[1], bad[0][1][0], bad[0][1][1])
+    for t in rows:
+        assert np.array_equal(u32(tabs[t].values.cpu().numpy()), u32(want[t])), t
+
+
 def test_stage_chain_verifies_on_device(ds, golden):
     """Restore-side checksums on the device (store.py:488-507): a good chain
     restores exactly like restore_chain; one flipped byte raises
