@@ -936,8 +936,10 @@ def run_restore(args):
         hs, descs = rank_slices(h, infos, kind != "full", [ranges[i.table_id] for i in infos])
         pin = torch.from_numpy(hs).pin_memory()
         slices.append((kind, h, pin, pin.to(dev), descs))
-    rows_restored = sum(hi - lo for lo, hi in ranges.values())  # a full section restores every row
-    rows_restored_all = sum(cards)
+    rows_restored = sum(hi - lo for lo, hi in ranges.values())  # this rank's rows
+    # records the chain restores (all ranks): every row of the full section
+    # plus every incremental record -- each is unpacked, dequantized, scattered
+    chain_records = sum(i.rows for kind, h in host for i in parse_headers(h, kind != "full"))
     chain_records_rank = sum(d[1] for kind, _, _, _, descs in slices for d in descs
                              if kind != "full") + rows_restored
 
@@ -1012,8 +1014,7 @@ def run_restore(args):
             parity["mismatches"], parity["rows_checked"] = int(mm[0].item()), int(mm[1].item())
     h2d = sum(p.numel() for _, _, p, _, _ in slices)
     full_bytes = sum(len(h) for _, h in host)
-    nbytes = rows_restored_all * dim * 4  # restored rows of all ranks (full section: every row)
-    rec = [i.record_size for i in parse_headers(host[0][1], False)][0]
+    nbytes = chain_records * dim * 4  # restored row bytes of all ranks
     # roofline: this rank's algorithmic bytes = its slices read + its restored
     # fp32 rows written (every record of the rank is applied once per payload)
     alg = h2d + chain_records_rank * dim * 4
@@ -1027,14 +1028,20 @@ def run_restore(args):
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8->f32 via f64",
             "data": "synthetic",
-            "config": dict(workload_desc(w), chain_payload_bytes=full_bytes,
+            "config": dict(workload_desc(w), chain_records=chain_records, chain_payload_bytes=full_bytes,
                            rank_upload_bytes=h2d, rows_per_rank=rows_restored,
                            parallelism=f"row-sharded x{world} (rank-local slices)",
                            timing="CUDA events at each chain's bounds, max over ranks"),
             "roofline": {"bound": "hbm",
                          "kernel": "ds::restore_payload_kernel (one launch per payload of the chain)",
                          "achieved": alg / t / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": alg / t / 1e9 / peak, "traffic": None},
+                         "frac": alg / t / 1e9 / peak,
+                         "traffic": (json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+                                     .get("C5", {}).get("restore_chain")
+                                     if os.path.exists(os.path.join(ROOT, "profiles", "traffic.json"))
+                                     else None),
+                         "traffic_note": "dram read+write bytes of the chain's launches (ncu --set full), "
+                                         "per chain"},
             "e2e": {"value": nbytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 4 * len(host) * len(cards)},
             "parity": parity,

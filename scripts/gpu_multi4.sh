@@ -1,0 +1,9 @@
+#!/bin/bash
+# 4-GPU round trip: the NCCL tests at 4 ranks, C2 weak scaling, C5 restore, the T shard x4
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+nvidia-smi topo -m > gpurun_out/topo_n4.txt 2>&1
+timeout 900 python -m pytest tests/test_multi_gpu.py -m gpu -q 2>&1 | tail -3
+R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
+timeout 900 $R --master-port 29611 bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/m_C2_n4.json 2> gpurun_out/m_C2_n4.err; echo "C2 n=4 rc=$?"
+timeout 900 $R --master-port 29612 bench.py --workload C5 --gpus 4 --steps 10 --warmup 3 > gpurun_out/m_C5_n4.json 2> gpurun_out/m_C5_n4.err; echo "C5 n=4 rc=$?"
+timeout 1500 $R --master-port 29613 bench.py --workload T --gpus 4 --steps 10 --warmup 3 > gpurun_out/m_T_n4.json 2> gpurun_out/m_T_n4.err; echo "T n=4 rc=$?"

@@ -5,7 +5,9 @@ global Zipf-like lookup stream, runs K2 + the count exchange (NVLink peer
 stores, or the NCCL all_gather with DS_COUNTS_EXCHANGE=nccl) + K3
 (ShardedCheckpointer.step; the second of three intervals staged), and rank 0
 assembles the shard payload from every rank's D2H'd runs.  It must equal the oracle's single-process payload of the
-whole tables (engine.py:118-189) byte for byte.
+whole tables (engine.py:118-189) byte for byte.  Then every rank restores
+its rows of a full + 2 incremental chain from rank-local uploads
+(engine.rank_slices) and checks them against the oracle's restore.
 """
 import os
 import sys
@@ -80,6 +82,54 @@ def main():
             if blob != ref:
                 ok = False
                 print(f"MISMATCH interval {interval}: {len(blob)} {len(ref)}", flush=True)
+    # rank-local restore of a full + 2 incremental chain (SURVEY 8(e) "Restore"):
+    # every rank restores its rows, uploading only its records; its rows and
+    # since-baseline bits equal the oracle's restore of the whole chain
+    if bitwidth is not None:
+        import paper_2010_08679_b200 as ds
+        from paper_2010_08679_b200.engine import apply_payload
+        vals = {t: v.copy() for t, v in full.items()}
+        chain = [("full", O.build_shard_payload({t: (v, None) for t, v in vals.items()}, "full", None,
+                                                bitwidth, sorted(ROWS))[0])]
+        for k in range(2):
+            sel = {t: np.unique(rng.integers(0, r, max(1, r // 4))) for t, r in ROWS.items()}
+            for t in ROWS:
+                vals[t] = vals[t] + np.float32(0.5)
+            chain.append(("incremental", O.build_shard_payload(
+                {t: (v, None) for t, v in vals.items()}, "incremental", sel, bitwidth, sorted(ROWS))[0]))
+        want = {t: np.zeros((r, dim), np.float32) for t, r in ROWS.items()}
+        bits = {t: np.zeros((r + 7) // 8, np.uint8) for t, r in ROWS.items()}
+        for kind, blob in chain:
+            inc = kind == "incremental"
+            for tid, sec in O.split_sections(blob, inc):
+                O.apply_section(sec, inc, want[tid], None, bits[tid] if inc else None)
+        out = {t.table_id: ds.DeviceTable(t.table_id, torch.zeros_like(t.values), row_base=t.row_base,
+                                          total_rows=t.total_rows) for t in tables}
+        tr = ds.ModelTracker({t: o.rows for t, o in out.items()}, device=dev)
+        up = 0
+        for kind, blob in chain:
+            inc = kind == "incremental"
+            apply_payload(blob, inc, out, {t: tr.baseline_bitmap(t) for t in out} if inc else None,
+                          device=dev)
+            up += apply_payload.last_h2d_bytes
+        torch.cuda.synchronize()
+        for t, o in out.items():
+            lo, hi = o.row_base, o.row_base + o.rows
+            if not np.array_equal(o.values.cpu().numpy().view(np.uint32), want[t][lo:hi].view(np.uint32)):
+                ok = False
+                print(f"RESTORE MISMATCH rank {rank} table {t}", flush=True)
+            rb = np.unpackbits(bits[t], bitorder="little")[:ROWS[t]][lo:hi]
+            gb = np.unpackbits(tr.baseline_bitmap(t).to_bytes(), bitorder="little")[:hi - lo]
+            if not np.array_equal(rb, gb):
+                ok = False
+                print(f"BASELINE MISMATCH rank {rank} table {t}", flush=True)
+        total = sum(len(b) for _, b in chain)
+        if up > total * (1.0 / world + 0.05):
+            ok = False
+            print(f"rank {rank} uploaded {up} of {total} chain bytes", flush=True)
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        ok = all(oks)
     if rank == 0 and ok:
         print("OK", flush=True)
     dist.barrier()
