@@ -395,22 +395,19 @@ def apply_payload(data, incremental: bool, tables: dict, baseline: dict | None =
         while (k1 < napply and k1 - k0 < _lib.MAX_TABLES and
                (infos[k1].dim, infos[k1].bitwidth, infos[k1].aux) == key):
             k1 += 1
-        secs = (_lib.RestoreSec * (k1 - k0))()
+        # ds_restore_sec rows (9 x 64-bit fields, include/deltasnap_cuda.h)
+        secs = np.empty((k1 - k0, 9), dtype=np.int64)
         for j, info in enumerate(infos[k0:k1]):
             t = tables[info.table_id]
             bm = baseline.get(info.table_id) if (baseline is not None and incremental) else None
-            secs[j].body_off = body_off[k0 + j]
-            secs[j].nrec = nrec[k0 + j]
             # a rank may hold no rows of a table: any valid address (nothing is written)
-            secs[j].values = t.values.data_ptr() or _dummy_rows(dev).data_ptr()
-            secs[j].aux_values = t.aux.data_ptr() if (info.aux and t.aux is not None) else None
-            secs[j].baseline = None if bm is None else bm.words.data_ptr()
-            secs[j].ld = t.values.stride(0)
-            secs[j].table_rows = t.total_rows
-            secs[j].row_lo = t.row_base
-            secs[j].row_hi = t.row_base + t.rows
+            secs[j] = (body_off[k0 + j], nrec[k0 + j],
+                       t.values.data_ptr() or _dummy_rows(dev).data_ptr(),
+                       t.aux.data_ptr() if (info.aux and t.aux is not None) else 0,
+                       0 if bm is None else bm.words.data_ptr(),
+                       t.values.stride(0), t.total_rows, t.row_base, t.row_base + t.rows)
         _lib.check(L.ds_restore_payload(
-            buf.data_ptr(), ctypes.cast(secs, ctypes.c_void_p), k1 - k0, key[0], key[1] or 0,
+            buf.data_ptr(), secs.ctypes.data, k1 - k0, key[0], key[1] or 0,
             int(key[2]), int(incremental), flags[k0:].data_ptr(), stream), "restore_payload")
         k0 = k1
 

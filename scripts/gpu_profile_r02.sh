@@ -15,5 +15,10 @@ run() {  # name, ncu filter, skip, count, command...
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --verify-rows 0"
 run C2 "mark_tma|cap3|writer_warp" 12 4 $B
 run T "writer_warp" 3 1 $B --workload T
+run C4 "writer_warp" 3 1 $B --workload C4
 run C5 "restore_payload" 18 6 python bench.py --workload C5 --steps 2 --warmup 3 --verify-rows 0
 NB=500 SORTED=1 FULLK=train_interval run train "train_|sort_" 0 1 python scripts/bench_train.py
+# the reports are too large to travel (gpurun_out <= 64 MiB): summarise here
+PROFILE_OUT=$OUT python scripts/make_profiles_r02.py r02 > $OUT/make_profiles.log 2>&1; echo "summary rc=$?"
+for f in $OUT/p_*.ncu-rep; do ncu -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done
+rm -f $OUT/p_*.ncu-rep
