@@ -342,14 +342,26 @@ __global__ void __launch_bounds__(256) train_interval_kernel(const TrainIArgs a)
                     if (do_aux) aac = tb.aux[r * tb.ld + e];
                 }
                 const float *ds = a.dsorted + (int64_t)e;
-                for (int64_t m = hp; m < re; m += 32) {
-                    const int cnt = (int)min((int64_t)32, re - m);
+                int64_t m = hp;
+                for (; m + 32 <= re; m += 32) {  // full chunks: 32 loads in flight per lane
                     float dl[32];
 #pragma unroll
-                    for (int j = 0; j < 32; j++) dl[j] = (j < cnt && on) ? __ldg(ds + (m + j) * d) : 0.f;
+                    for (int j = 0; j < 32; j++) dl[j] = on ? __ldg(ds + (m + j) * d) : 0.f;
 #pragma unroll
-                    for (int j = 0; j < 32; j++)
-                        if (j < cnt) {  // np.add.at order
+                    for (int j = 0; j < 32; j++) {  // np.add.at order
+                        if (do_val) acc = __fadd_rn(acc, dl[j]);
+                        if (do_aux) aac = __fadd_rn(aac, __fmul_rn(dl[j], dl[j]));
+                    }
+                }
+                // the tail (most runs are 1-3 updates long): 4 at a time
+                for (; m < re; m += 4) {
+                    const int cnt = (int)min((int64_t)4, re - m);
+                    float dl[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) dl[j] = (j < cnt && on) ? __ldg(ds + (m + j) * d) : 0.f;
+#pragma unroll
+                    for (int j = 0; j < 4; j++)
+                        if (j < cnt) {
                             if (do_val) acc = __fadd_rn(acc, dl[j]);
                             if (do_aux) aac = __fadd_rn(aac, __fmul_rn(dl[j], dl[j]));
                         }
@@ -393,26 +405,39 @@ __global__ void __launch_bounds__(TL_THREADS) train_long_kernel(const TrainIArgs
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp > 0) {
-        // producers: chunk c -> stage c % TL_STAGES once the consumer freed it
-        const int pt = threadIdx.x - 32, np = TL_THREADS - 32;
-        for (int64_t c = 0; c < nchunks; c++) {
+        // producers: warp w fills chunks w-1, w-1+7, ... (one chunk in flight
+        // per warp, no CTA barrier), each into stage c % TL_STAGES once the
+        // consumer released that stage's previous chunk
+        const int npw = TL_THREADS / 32 - 1;
+        for (int64_t c = warp - 1; c < nchunks; c += npw) {
             const int st = (int)(c % TL_STAGES);
-            if (pt == 0)
-                while (consumed + TL_STAGES <= c) __nanosleep(32);  // the stage's old chunk is done
-            asm volatile("bar.sync 1, %0;" ::"r"(np));
+            if (lane == 0)
+                while (consumed + TL_STAGES <= c) __nanosleep(32);
+            __syncwarp();
             const int64_t m0 = hp + c * TL_OCC;
             const int cnt = (int)min((int64_t)TL_OCC, hp + len - m0);
             const int nf = cnt * d;
             float *dst = ring + (size_t)st * TL_OCC * d;
             const float *src = a.dsorted + m0 * d;
-            if ((d & 3) == 0)
-                for (int i = pt; i < (nf >> 2); i += np)
-                    reinterpret_cast<float4 *>(dst)[i] = __ldg(reinterpret_cast<const float4 *>(src) + i);
-            else
-                for (int i = pt; i < nf; i += np) dst[i] = __ldg(src + i);
+            if ((d & 3) == 0) {
+                constexpr int U = TL_OCC * 32 / 4 / 32;  // float4 per lane of a full d32 chunk
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int i = lane + 32 * u;
+                    if (i < (nf >> 2)) v[u] = __ldg(reinterpret_cast<const float4 *>(src) + i);
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int i = lane + 32 * u;
+                    if (i < (nf >> 2)) reinterpret_cast<float4 *>(dst)[i] = v[u];
+                }
+            } else {
+                for (int i = lane; i < nf; i += 32) dst[i] = __ldg(src + i);
+            }
             __threadfence_block();
-            asm volatile("bar.sync 1, %0;" ::"r"(np));
-            if (pt == 0) filled[st] = (int)(c + 1);
+            __syncwarp();
+            if (lane == 0) filled[st] = (int)(c + 1);
         }
         return;
     }
