@@ -46,6 +46,13 @@ ZIPF_S = 1.05
 
 # BASELINE.json configs as single-GPU workloads (per-rank shards; weak scaling)
 WORKLOADS = {
+    # configs[0]: the reference's own CPU-runnable case (8 x 1M x 64, 1000
+    # batches of 2048 Zipf lookups per table, incremental, 4-bit uniform
+    # asymmetric = naive min/max ranges)
+    "C1": dict(desc="C1: synthetic DLRM-style 8 tables x 1M rows x dim 64 fp32, Zipf lookups, 1000 "
+                    "batches of 2048, incremental 4-bit uniform asymmetric (naive ranges)",
+               cards=[1_000_000] * 8, dim=64, bitwidth=4, adaptive=False, lookups="zipf",
+               n_per_table=1000 * BATCH),
     # configs[1]: the metric's headline config (the default)
     "C2": dict(desc="C2: Criteo-Kaggle-shaped 26 tables x dim 16 fp32, 8-bit naive, checkpoint "
                     "every 500 batches x 2048 Zipf(1.05) lookups/table",

@@ -1,6 +1,3 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 900 python -m pytest tests -m gpu -q -x --timeout=300 2>&1 | tail -3
-SORTED=1 timeout 300 python scripts/bench_train.py
-timeout 600 python scripts/bench_overlap.py
-timeout 600 python bench.py --workload C5 --steps 10 --warmup 3 --verify-rows 0 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('C5', d['value'], d['ms_per_step'], d['e2e']['value'])"
+REPS=1 WLS="C4 C3" VROWS=300000 BENCH_ARGS="--no-shipped" bash scripts/ab_env.sh "" "DS_CUDA_LIB=paper_2010_08679_b200/libdeltasnap_cuda_noties.so"

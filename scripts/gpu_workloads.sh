@@ -5,7 +5,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.csv 2>&1
 lscpu > gpurun_out/lscpu.txt 2>&1
-for wl in ${WORKLOADS:-C2 T T-adaptive C3 C4 C5}; do
+for wl in ${WORKLOADS:-C2 C1 T T-adaptive C3 C4 C5}; do
   timeout 1200 python bench.py --workload $wl --steps ${STEPS:-10} --warmup 3 ${EXTRA:-} > gpurun_out/w_$wl.json 2> gpurun_out/w_$wl.err
   echo "$wl rc=$?"
 done

@@ -9,7 +9,7 @@ def last_json(p):
     return json.loads(open(p).read().strip().splitlines()[-1])
 
 
-for wl in ["C2", "T", "T-adaptive", "C3", "C4", "C5"]:
+for wl in ["C2", "C1", "T", "T-adaptive", "C3", "C4", "C5"]:
     p = f"gpurun_out/w_{wl}.json"
     if not os.path.exists(p):
         continue
