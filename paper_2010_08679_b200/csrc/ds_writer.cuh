@@ -21,6 +21,9 @@
 #ifndef DS_ERR_F2F
 #define DS_ERR_F2F 1  // 1: the err_sum term through the conversion unit; 0: err_fast (integer bits)
 #endif
+#ifndef DS_TT_BALLOT
+#define DS_TT_BALLOT 0  // 1: strided tiles find their table by ballot (measured 2 us slower at C2)
+#endif
 #ifndef DS_M1_FUSED
 #define DS_M1_FUSED 1  // naive 2/4/8-bit rows: codes packed as produced (code_row_m1)
 #endif
@@ -997,8 +1000,12 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
             TI r;
             const int64_t tile = tbeg + (int64_t)j * tstep;
             r.ok = tile < tend;
-            if (r.ok)
-                while (tcur + 1 < nt && s_sched[tcur + 1] <= tile) tcur++;  // warp-uniform
+            if (r.ok) {
+                // warp-uniform: runs of tiles step table by table; strided
+                // tiles can jump many small tables -- one ballot per 32 tables
+                if (RUN || !DS_TT_BALLOT) while (tcur + 1 < nt && s_sched[tcur + 1] <= tile) tcur++;
+                else tcur = tile_table(s_sched, nt, tile, lane);
+            }
             r.t = r.ok ? tcur : 0;
             r.i0 = r.ok ? (tile - s_sched[r.t]) * TR : 0;
             r.nrow = r.ok ? (int)min((int64_t)TR, s_sched[nt + 1 + r.t] - r.i0) : 0;

@@ -136,9 +136,9 @@ class TrainingCheckpointLoop:
     stream (ShardedCheckpointer.checkpoint(staged_rows=...)); K3 then runs
     from the staged copy on a side stream, and a background thread waits for
     it and issues the pinned D2H on a copy stream -- the training steps never
-    wait for either.  Payload slots are double-buffered; the compute stream
-    only waits for the D2H of the checkpoint two intervals back before its
-    slot is rewritten.
+    wait for either.  Payload slots are double-buffered; checkpoint() waits
+    (on the host) only for the D2H of the checkpoint two intervals back
+    before its slot is rewritten -- normally long complete.
 
         loop = TrainingCheckpointLoop(ck, staged_rows)
         for interval in ...:
@@ -214,14 +214,18 @@ class TrainingCheckpointLoop:
         # normally long done, the host wait is then immediate
         self._free[s].wait()
         self._free[s].clear()
-        self.ck.payload = self.payload[s]
-        stall_end = self.ck.checkpoint(staged_rows=self.staged_rows)
-        side = self.ck._side
-        with torch.cuda.stream(side):
-            self.meta[s, 0:1].copy_(self.ck.writer.sec_off[-1:], non_blocking=True)
-            self.meta[s, 1:2].copy_(self.ck.writer.flags.to(torch.int64), non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(side)
+        try:
+            self.ck.payload = self.payload[s]
+            stall_end = self.ck.checkpoint(staged_rows=self.staged_rows)
+            side = self.ck._side
+            with torch.cuda.stream(side):
+                self.meta[s, 0:1].copy_(self.ck.writer.sec_off[-1:], non_blocking=True)
+                self.meta[s, 1:2].copy_(self.ck.writer.flags.to(torch.int64), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        except BaseException:
+            self._free[s].set()  # nothing was queued for this slot
+            raise
         self._q.put((s, ev))
         self.k += 1
         return stall_end
