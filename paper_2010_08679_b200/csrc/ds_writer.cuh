@@ -21,6 +21,10 @@
 #ifndef DS_ERR_F2F
 #define DS_ERR_F2F 1  // 1: the err_sum term through the conversion unit; 0: err_fast (integer bits)
 #endif
+#ifndef DS_M1_ERR
+#define DS_M1_ERR 1  // naive rows' err term: 0 F2F for q and the level, 1 q by the 2^52 magic
+                     // (DADD; T shard 6.98 -> 6.61 ms), 2 also the level rounded by integer bits
+#endif
 #ifndef DS_TT_BALLOT
 #define DS_TT_BALLOT 0  // 1: strided tiles find their table by ballot (measured 2 us slower at C2)
 #endif
@@ -266,9 +270,13 @@ __device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x
             dev = fmaxf(dev, fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))));
             const bool in = !PAD || el(k) < d;
 #if DS_ERR_F2F
-            const double er = __dsub_rn((double)x[k],
-                                        (double)__double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)__uint_as_float(
-                                            __float_as_uint(__fsub_rn(qm, 12582912.0f)))), lod)));
+            // x - f32(RN(RN(s*q) + lo)), exact in f64 (DS_M1_ERR: how q enters
+            // f64 and how the level is rounded to f32 -- same value)
+            const double qd = DS_M1_ERR >= 1 ? code_to_f64(qi)
+                                             : (double)__fsub_rn(qm, 12582912.0f);
+            const double wv = __dadd_rn(__dmul_rn(rq.s, qd), lod);
+            const double dq = DS_M1_ERR >= 2 ? round_f32_in_f64(wv) : (double)__double2float_rn(wv);
+            const double er = __dsub_rn((double)x[k], dq);
 #else
             const double er = err_fast(x[k], qi, rq.s, lod);  // engine.py:171-173
 #endif
@@ -419,7 +427,8 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
                 dev = fmaxf(dev, fabsf(__fsub_rn(v, qf)));
                 // err_sum term (engine.py:171-173): exact dequantized value
 #if DS_ERR_F2F
-                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, (double)qf), lod));
+                const double qd = DS_M1_ERR >= 1 ? code_to_f64((uint32_t)q[k]) : (double)qf;
+                const float dq = __double2float_rn(__dadd_rn(__dmul_rn(rq.s, qd), lod));
                 const double er = __dsub_rn((double)x[k], (double)dq);
 #else
                 const double er = err_fast(x[k], (uint32_t)q[k], rq.s, lod);
