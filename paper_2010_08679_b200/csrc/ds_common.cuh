@@ -325,9 +325,9 @@ static __device__ double pw_sum(const double *a, int n) {
 // Lanes whose group has want == false still take part in the syncs.
 // ---------------------------------------------------------------------------
 template <int G, int C, int VEC>
-__device__ __noinline__ double exact_me_group(const float (&x)[C * VEC], int d, int lig,
-                                              float lo, float hi, int L, bool want,
-                                              double *buf, unsigned &nexact_codes) {
+__device__ __forceinline__ double exact_me_impl(const float (&x)[C * VEC], int d, int lig,
+                                                float lo, float hi, int L, bool want,
+                                                double *buf, unsigned &nexact_codes) {
     using Lay = Layout<G, C, VEC>;
     constexpr int EPL = C * VEC;
     if (want) {
@@ -370,6 +370,61 @@ __device__ __noinline__ double exact_me_group(const float (&x)[C * VEC], int d, 
     int lane = threadIdx.x & 31;
     res = __shfl_sync(DS_FULL_MASK, res, lane & ~(G - 1));
     return __dsqrt_rn(res);
+}
+
+template <int G, int C, int VEC>
+__device__ __noinline__ double exact_me_group(const float (&x)[C * VEC], int d, int lig,
+                                              float lo, float hi, int L, bool want,
+                                              double *buf, unsigned &nexact_codes) {
+    return exact_me_impl<G, C, VEC>(x, d, lig, lo, hi, L, want, buf, nexact_codes);
+}
+
+// the same from the group's row in shared memory (Layout order at `row`)
+template <int G, int C, int VEC>
+__device__ __noinline__ double exact_me_row(const float *row, int d, int lig, float lo, float hi,
+                                            int L, bool want, double *buf, unsigned &nexact_codes) {
+    using Lay = Layout<G, C, VEC>;
+    float x[C * VEC];
+#pragma unroll
+    for (int k = 0; k < C * VEC; k++) {
+        const int e = Lay::elem(lig, k);
+        x[k] = e < d ? row[e] : 0.f;
+    }
+    return exact_me_impl<G, C, VEC>(x, d, lig, lo, hi, L, want, buf, nexact_codes);
+}
+
+// ---------------------------------------------------------------------------
+// packed fp32 pairs (sm_100a FADD2 / FMUL2 / FFMA2: two lanes of fp32 per
+// instruction, IEEE round-to-nearest like the scalar ops)
+// ---------------------------------------------------------------------------
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void up2(f32x2 v, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -420,6 +475,9 @@ __device__ __forceinline__ void eval_fast(const float (&x)[C * VEC], int d, int 
 #ifndef DS_GREEDY_NO_TIES
 #define DS_GREEDY_NO_TIES 0
 #endif
+#ifndef DS_GREEDY_PACKED
+#define DS_GREEDY_PACKED 1  // both candidates in packed fp32 pairs (FADD2/FMUL2/FFMA2)
+#endif
 template <int G, int C, int VEC, bool PAD>
 __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int lig, float loA,
                                            float hiA, float loB, float hiB, int L, float &SA,
@@ -434,6 +492,35 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
     const float invB = okB ? __fdividef((float)L, rngB) : 0.f;
     const float sA = __fmul_rn(rngA, 1.0f / (float)L), sB = __fmul_rn(rngB, 1.0f / (float)L);
     float sseA = 0.f, sseB = 0.f, rmA = 0.f, rmB = 0.f;
+#if DS_GREEDY_PACKED
+    // both candidates in the two halves of packed fp32 pairs: the same
+    // roundings as the scalar loop below (rint as the 1.5*2^23 magic add:
+    // round half to even for v in [0, L(1+5u)])
+    {
+        const f32x2 LO = pk2(loA, loB), INV = pk2(invA, invB), S2 = pk2(sA, sB);
+        const f32x2 MAG = pk2(12582912.0f, 12582912.0f);
+        f32x2 sse = pk2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < EPL; k++) {
+            const float cA = fminf(fmaxf(x[k], loA), hiA);
+            const float cB = fminf(fmaxf(x[k], loB), hiB);
+            const f32x2 v = mul2(sub2(pk2(cA, cB), LO), INV);
+            const f32x2 q = sub2(add2(v, MAG), MAG);
+            float rA, rB;
+            up2(sub2(v, q), rA, rB);
+            if (!DS_GREEDY_NO_TIES) {
+                rmA = fmaxf(rmA, fabsf(rA));
+                rmB = fmaxf(rmB, fabsf(rB));
+            } else {
+                rmA = rmB = 1.f;
+            }
+            f32x2 e = sub2(pk2(x[k], x[k]), fma2(q, S2, LO));
+            if (PAD && !(Lay::elem(lig, k) < d)) e = pk2(0.f, 0.f);
+            sse = fma2(e, e, sse);
+        }
+        up2(sse, sseA, sseB);
+    }
+#else
 #pragma unroll
     for (int k = 0; k < EPL; k++) {
         const float cA = fminf(fmaxf(x[k], loA), hiA);
@@ -457,6 +544,7 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
         sseA = __fmaf_rn(eA, eA, sseA);
         sseB = __fmaf_rn(eB, eB, sseB);
     }
+#endif
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
         sseA += __shfl_xor_sync(DS_FULL_MASK, sseA, o, G);

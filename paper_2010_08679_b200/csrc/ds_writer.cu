@@ -14,17 +14,18 @@ struct WarpPlan {
 };
 static WarpPlan warp_plan(int d, int64_t rec, const Cfg &c, int mode = 1) {
     const int rpc = 32 / c.G;
-    const int ns = c.G == 1 ? DS_WRITER_NS1 : DS_WRITER_NS;  // writer_stages<G>()
+    const int ns = mode == 2 ? DS_WRITER_NS_GREEDY : (c.G == 1 ? DS_WRITER_NS1 : DS_WRITER_NS);
     auto warp_bytes = [&](int trr) {
         return (size_t)align16((int)(trr * rec)) + 16 + align16(rpc * d) +
                (size_t)ns * ((rpc * d * 4 + 63) & ~63) +
-               (mode == 2 ? (size_t)align16(rpc * (d + 8) * 8) : 0);
+               (mode == 2 ? (size_t)align16(rpc * greedy_scratch_bytes(c.G * c.C * c.VEC, d)) : 0);
     };
     WarpPlan p;
     p.tr = 32;
-    while (warp_bytes(p.tr) * (DS_WT_WARP / 32) > 200 * 1024 && p.tr / 2 >= rpc * (ns - 1) && p.tr > 1)
+    const int wt = mode == 2 ? DS_WT_GREEDY : DS_WT_WARP;
+    while (warp_bytes(p.tr) * (wt / 32) > 200 * 1024 && p.tr / 2 >= rpc * (ns - 1) && p.tr > 1)
         p.tr /= 2;
-    p.threads = DS_WT_WARP;
+    p.threads = wt;
     while (warp_bytes(p.tr) * (p.threads / 32) > 200 * 1024 && p.threads > 32) p.threads /= 2;
     p.smem = warp_bytes(p.tr) * (p.threads / 32) + 16;  // + alignment slack
     return p;
@@ -279,7 +280,7 @@ extern "C" int ds_write_payload(const ds_table_desc *tables_host, int ntables,
         const int rpp = WT / c.G;  // one pass of rows per tile (compute-bound)
         tr = rpp;
         smem = (size_t)align16(tr * a.rec) + 16 + align16(rpp * d) +
-               (size_t)rpp * (d + 8) * sizeof(double);
+               (size_t)rpp * greedy_scratch_bytes(c.G * c.C * c.VEC, d);
     }
     a.tile_rows = tr;
     if (smem > 200 * 1024) return host::fail(DS_ERR_CONFIG, "ds_write_payload: record too large");

@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include "ds_common.cuh"
+#include "ds_greedy.cuh"
 #include "ds_host.h"
 
 #ifndef DS_ERR_F2F
@@ -388,9 +389,18 @@ __device__ __forceinline__ bool code_row(const WriterArgs &a, const ds_table_des
         const bool row_ok = valid && fin;
         float lo = mn, hi = mx;
         if (!row_ok) { lo = 0.f; hi = 0.f; }
-        if (MODE == 2)
-            greedy_row<G, C, VEC, PAD>(x, d, lig, row_ok, lo, hi, L, a.bins, a.steps, buf, lo, hi,
-                                       acc.n_exact_dec, acc.n_exact_codes);
+        if (MODE == 2) {
+            if constexpr (DS_GREEDY_BUCKET) {
+                // the row stays in the ring stage (xs): re-read after the search
+                greedy_row_bucket<G, C, VEC, PAD>(xs, d, lig, row_ok, lo, hi, L, a.invL, a.bins, a.steps,
+                                                  reinterpret_cast<uint8_t *>(buf), lo, hi,
+                                                  acc.n_exact_dec, acc.n_exact_codes);
+#pragma unroll
+                for (int k = 0; k < EPL; k++) x[k] = (valid && el(k) < d) ? xs[el(k)] : 0.f;
+            } else
+                greedy_row<G, C, VEC, PAD>(x, d, lig, row_ok, lo, hi, L, a.bins, a.steps, buf, lo, hi,
+                                           acc.n_exact_dec, acc.n_exact_codes);
+        }
         const RowQ rq = make_rowq(lo, hi, L, a.invL);
         bool fused = false;
         if constexpr (MODE == 1 && VEC == 4 && DS_M1_FUSED && G > 1) {  // one-lane rows: measured slower
@@ -937,19 +947,29 @@ __device__ __forceinline__ int chunk_swz(int g) { return g ^ ((g >> 3) & 3); }
 template <int G>
 __host__ __device__ constexpr int writer_stages() { return G == 1 ? DS_WRITER_NS1 : DS_WRITER_NS; }
 
+// the greedy writer's CTA: 256 threads at 2 CTAs/SM (128 registers) for the
+// fp32 candidate passes; the bucketed search (DS_GREEDY_BUCKET=1) needs 4 KB
+// more shared memory per row: 128 threads at 3 CTAs/SM, a 2-stage ring
 #ifndef DS_WRITER_MINB_GREEDY
-#define DS_WRITER_MINB_GREEDY 2
+#define DS_WRITER_MINB_GREEDY (DS_GREEDY_BUCKET ? 3 : 2)
+#endif
+#ifndef DS_WT_GREEDY
+#define DS_WT_GREEDY (DS_GREEDY_BUCKET ? 128 : 256)
+#endif
+#ifndef DS_WRITER_NS_GREEDY
+#define DS_WRITER_NS_GREEDY (DS_GREEDY_BUCKET ? 2 : 3)
 #endif
 #ifndef DS_WT_WARP
 #define DS_WT_WARP WT  // threads per CTA of the warp-pipelined writer
 #endif
 template <int G, int C, int VEC, int MODE, bool PAD>
-__global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
+__global__ void __launch_bounds__(MODE == 2 ? DS_WT_GREEDY : DS_WT_WARP,
+                                  MODE == 2 ? DS_WRITER_MINB_GREEDY : DS_WRITER_MINB)
     writer_warp_kernel(const WriterArgs a) {
     pdl_wait();  // K2's ids and counts (PDL launch after the emit pass)
     constexpr int EPL = C * VEC;
     constexpr int RPC = 32 / G;  // rows per chunk
-    constexpr int NS = writer_stages<G>();
+    constexpr int NS = MODE == 2 ? DS_WRITER_NS_GREEDY : writer_stages<G>();
     // one-lane rows re-code flagged rows in place (measured faster); wider
     // groups keep the after-loop pass (fewer live registers in the hot loop)
     constexpr bool FIXIN = DS_FIX_INLINE && G == 1;
@@ -964,7 +984,11 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
     const int stage_b = align16(TR * a.rec) + 16;
     const int codes_b = align16(RPC * d);
     const int chunk_b = (RPC * d * 4 + 63) & ~63;  // whole 4-chunk swizzle groups
-    const int exact_b = MODE == 2 ? align16(RPC * (d + 8) * 8) : 0;  // greedy exact scratch
+    // greedy scratch per row: the bucket sort + prefix sums (ds_greedy.cuh),
+    // which the exact re-evaluation also borrows
+    static_assert(bucket_bytes(G * EPL) == BucketLayout<G * EPL>::BYTES, "host and device scratch sizes");
+    const int gscr = greedy_scratch_bytes(G * EPL, d);
+    const int exact_b = MODE == 2 ? align16(RPC * gscr) : 0;
     const int warp_b = stage_b + codes_b + NS * chunk_b + exact_b;
     uint8_t *smem_al = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem) + 15) & ~(uintptr_t)15);
     uint8_t *wbase = smem_al + (size_t)wid * warp_b;
@@ -1114,7 +1138,7 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
                 }
                 const bool fix = code_row<G, C, VEC, MODE, PAD, VEC == 4 && G == 1>(a, td, x, row, valid, valid ? loc : 0,
                                                                 stage + r * a.rec, codes + slot * d,
-                                                                exact + slot * (d + 8), lig, d, acc);
+                                                                exact + slot * (gscr / 8), lig, d, acc);
                 if (MODE == 1 && FIXIN) {
                     // exact fixup now, from the registers (no second pass)
                     if (__any_sync(DS_FULL_MASK, fix))
@@ -1164,6 +1188,7 @@ __global__ void __launch_bounds__(DS_WT_WARP, MODE == 2 ? DS_WRITER_MINB_GREEDY 
 // ---------------------------------------------------------------------------
 template <int G, int C, int VEC, int MODE, bool PAD>
 __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
+    static_assert(!(MODE == 2 && DS_GREEDY_BUCKET), "the bucketed search reads rows from the warp writer's ring");
     pdl_wait();
     constexpr int EPL = C * VEC;
     constexpr int RPP = WT / G;  // rows per pass
@@ -1173,7 +1198,8 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
     const int stage_bytes = align16(TR * a.rec) + 16;
     uint8_t *stage = smem;
     uint8_t *codes_sh = smem + stage_bytes;                                 // RPP * d bytes
-    double *exact_sh = reinterpret_cast<double *>(codes_sh + align16(RPP * d));  // RPP*(d+8)
+    const int gscr = greedy_scratch_bytes(G * EPL, d);  // per row: the greedy scratch
+    double *exact_sh = reinterpret_cast<double *>(codes_sh + align16(RPP * d));
 
     __shared__ int64_t s_sched[3 * DS_MAX_TABLES + 2];
     __shared__ double s_red[WT / 32];
@@ -1215,7 +1241,7 @@ __global__ void __launch_bounds__(WT, 1) writer_kernel(const WriterArgs a) {
 #pragma unroll
                     for (int k = 0; k < EPL; k++) x[k] = 0.f;
                 code_row<G, C, VEC, MODE, PAD>(a, td, x, nullptr, valid, local, stage + r * a.rec,
-                                               codes_sh + slot * d, exact_sh + slot * (d + 8), lig,
+                                               codes_sh + slot * d, exact_sh + slot * (gscr / 8), lig,
                                                d, acc);
             }
             __syncthreads();
@@ -1253,9 +1279,12 @@ static int next_pow2(int v) {
 #endif
 // mode 2 (greedy search) keeps ~16 elements per lane (register-bound); the
 // HBM-bound naive/fp32 writer amortises per-row work over DS_EPL_NAIVE
+#ifndef DS_EPL_GREEDY
+#define DS_EPL_GREEDY 16
+#endif
 static Cfg pick_cfg(int d, bool vec4, int mode = 2) {
     Cfg c;
-    const int epl = mode == 2 ? 16 : DS_EPL_NAIVE;
+    const int epl = mode == 2 ? DS_EPL_GREEDY : DS_EPL_NAIVE;
     if (vec4) {
         int chunks = d / 4;
         c.VEC = 4;
@@ -1284,6 +1313,12 @@ static writer_fn select_writer(const Cfg &c) {
     if constexpr (MODE != 2) {
         DS_W(1, 8, 4) DS_W(2, 8, 4) DS_W(4, 8, 4) DS_W(8, 8, 4) DS_W(16, 8, 4)
     }
+#if DS_EPL_GREEDY == 8
+    if constexpr (MODE == 2) {
+        DS_W(2, 2, 4) DS_W(4, 2, 4) DS_W(8, 2, 4) DS_W(16, 2, 4) DS_W(32, 2, 4)
+        DS_W(1, 8, 1) DS_W(2, 8, 1) DS_W(4, 8, 1) DS_W(8, 8, 1) DS_W(16, 8, 1) DS_W(32, 8, 1)
+    }
+#endif
     DS_W(1, 1, 1) DS_W(1, 2, 1) DS_W(1, 4, 1) DS_W(1, 8, 1) DS_W(1, 16, 1) DS_W(2, 16, 1)
     DS_W(4, 16, 1) DS_W(8, 16, 1) DS_W(16, 16, 1) DS_W(32, 16, 1) DS_W(32, 32, 1)
 #undef DS_W
