@@ -493,9 +493,8 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
     const float sA = __fmul_rn(rngA, 1.0f / (float)L), sB = __fmul_rn(rngB, 1.0f / (float)L);
     float sseA = 0.f, sseB = 0.f, rmA = 0.f, rmB = 0.f;
 #if DS_GREEDY_PACKED
-    // both candidates in the two halves of packed fp32 pairs: the same
-    // roundings as the scalar loop below (rint as the 1.5*2^23 magic add:
-    // round half to even for v in [0, L(1+5u)])
+    // both candidates in the two halves of packed fp32 pairs (rint as the
+    // 1.5*2^23 magic add: round half to even for v in [0, L(1+5u)])
     {
         const f32x2 LO = pk2(loA, loB), INV = pk2(invA, invB), S2 = pk2(sA, sB);
         const f32x2 MAG = pk2(12582912.0f, 12582912.0f);
@@ -504,10 +503,14 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
         for (int k = 0; k < EPL; k++) {
             const float cA = fminf(fmaxf(x[k], loA), hiA);
             const float cB = fminf(fmaxf(x[k], loB), hiB);
-            const f32x2 v = mul2(sub2(pk2(cA, cB), LO), INV);
-            const f32x2 q = sub2(add2(v, MAG), MAG);
+            // the product fused into the rounding and the distance (ptxas
+            // contracts f32x2 mul+add anyway; explicit FMAs make it defined):
+            // |t*inv - v_ref| is within the bound's epsw like the rounded v
+            const f32x2 t = sub2(pk2(cA, cB), LO);
+            const f32x2 qm = fma2(t, INV, MAG);
+            const f32x2 q = sub2(qm, MAG);
             float rA, rB;
-            up2(sub2(v, q), rA, rB);
+            up2(fma2(t, INV, sub2(MAG, qm)), rA, rB);
             if (!DS_GREEDY_NO_TIES) {
                 rmA = fmaxf(rmA, fabsf(rA));
                 rmB = fmaxf(rmB, fabsf(rB));

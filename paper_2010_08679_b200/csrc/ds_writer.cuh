@@ -19,6 +19,9 @@
 #include "ds_greedy.cuh"
 #include "ds_host.h"
 
+#ifndef DS_M1_PACKED
+#define DS_M1_PACKED 1  // naive rows: codes and the tie check in packed fp32 pairs
+#endif
 #ifndef DS_ERR_F2F
 #define DS_ERR_F2F 1  // 1: the err_sum term through the conversion unit; 0: err_fast (integer bits)
 #endif
@@ -259,16 +262,42 @@ __device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x
 #pragma unroll
     for (int c = 0; c < C; c++) {
         uint32_t pk = 0;
+#if DS_M1_PACKED
+        // the chunk's codes two at a time in packed fp32 pairs, the product
+        // fused (ptxas contracts f32x2 mul+add even with .rn, so it is written
+        // as FMAs and fix_tile mirrors exactly these): qm = RN(t*inv + 1.5*2^23)
+        // rounds the exact product t*inv half-to-even to the code, r =
+        // RN(t*inv - q) its distance; |t*inv - v_ref| <= 5u*L as for the
+        // rounded product, so the 8u*L guard band still certifies the code
+        float qms[4];
+        {
+            const f32x2 LO = pk2(rq.lo, rq.lo), INV = pk2(rq.inv, rq.inv);
+            const f32x2 MAG = pk2(12582912.0f, 12582912.0f);
+#pragma unroll
+            for (int j = 0; j < 4; j += 2) {
+                const f32x2 t = sub2(pk2(x[4 * c + j], x[4 * c + j + 1]), LO);
+                const f32x2 qm = fma2(t, INV, MAG);
+                float r0, r1;
+                up2(fma2(t, INV, sub2(MAG, qm)), r0, r1);  // MAG - qm = -q exactly
+                up2(qm, qms[j], qms[j + 1]);
+                dev = fmaxf(dev, fmaxf(fabsf(r0), fabsf(r1)));
+            }
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int k = 4 * c + j;
             // min/max ranges hold every element: no clip, v in [0, L(1+5u)];
             // round half to even through the 1.5*2^23 magic (low mantissa
             // bits = the code); |v - q| near 1/2 -> the exact fixup (RowQ)
+#if DS_M1_PACKED
+            const float qm = qms[j];
+#else
             const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
             const float qm = __fadd_rn(v, 12582912.0f);
-            const uint32_t qi = __float_as_uint(qm) & 0x3fffffu;
             dev = fmaxf(dev, fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))));
+#endif
+            const uint32_t qi = __float_as_uint(qm) & 0x3fffffu;
             const bool in = !PAD || el(k) < d;
 #if DS_ERR_F2F
             // x - f32(RN(RN(s*q) + lo)), exact in f64 (DS_M1_ERR: how q enters
@@ -849,17 +878,28 @@ __device__ __forceinline__ void fix_tile(const WriterArgs &a, const int64_t *s_s
         }
     const float lo = grp_min<G>(mn), hi = grp_max<G>(mx);
     const RowQ rq = make_rowq(lo, hi, a.L, a.invL);
-    // the hot loop's codes, exact codes for the ambiguous elements only
+    // the hot loop's codes (the packed code_row_m1 fuses the product, the
+    // generic path rounds it), exact codes for the ambiguous elements only
+    const bool fused = DS_M1_PACKED && DS_M1_FUSED && VEC == 4 && G > 1 &&
+                       (a.bitwidth == 8 || a.bitwidth == 4 || a.bitwidth == 2);
     int qfast[EPL], qex[EPL];
     bool changed = false;
 #pragma unroll
     for (int k = 0; k < EPL; k++) {
-        const float v = __fmul_rn(__fsub_rn(x[k], rq.lo), rq.inv);
-        const float qm = __fadd_rn(v, 12582912.0f);
+        const float t = __fsub_rn(x[k], rq.lo);
+        float qm, r;
+        if (fused) {
+            qm = __fmaf_rn(t, rq.inv, 12582912.0f);
+            r = __fmaf_rn(t, rq.inv, __fsub_rn(12582912.0f, qm));
+        } else {
+            const float v = __fmul_rn(t, rq.inv);
+            qm = __fadd_rn(v, 12582912.0f);
+            r = __fsub_rn(v, __fsub_rn(qm, 12582912.0f));
+        }
         qfast[k] = __float_as_int(qm) & 0x3fffff;
         qex[k] = qfast[k];
         const bool in = mine && (!PAD || Lay::elem(lig, k) < d);
-        if (in && (rq.mode == 2 || fabsf(__fsub_rn(v, __fsub_rn(qm, 12582912.0f))) > 0.5f - rq.eps)) {
+        if (in && (rq.mode == 2 || fabsf(r) > 0.5f - rq.eps)) {
             qex[k] = code_exact(x[k], lo, hi, rq.s, a.L);
             acc.n_exact_codes++;
             changed |= qex[k] != qfast[k];

@@ -430,6 +430,55 @@ def test_payload_dims_vs_oracle(ds, O, d, bw):
         assert err == pytest.approx(err_ref, rel=1e-12, abs=1e-300)
 
 
+def _near_tie_rows(rng, rows, d, L):
+    """Rows whose fp32 code product t*inv rounds to exactly k + 1/2 while the
+    exact product does not (t = RN(x - lo), inv = RN(RN(1/(hi - lo)) * L)):
+    the fused (FFMA) and the rounded code of such an element can differ, and
+    the reference's f64 code decides.  Found on the T workload (row 116128029:
+    v_ref = 13.500000137), kept here as a constructed regression."""
+    f32 = np.float32
+    out = np.empty((rows, d), f32)
+    for i in range(rows):
+        lo = f32(-1 + rng.uniform(0, 0.1))
+        hi = f32(1 - rng.uniform(0, 0.1))
+        x = rng.uniform(lo, hi, d).astype(f32)
+        x[0], x[1] = lo, hi
+        inv = f32(f32(f32(1) / f32(hi - lo)) * f32(L))
+        j = 2
+        for k in rng.permutation(L)[: min(L, 24)]:
+            x0 = f32(lo + f32((k + 0.5) / float(inv)))
+            for s in range(-8, 9):
+                xc = np.nextafter(x0, f32(np.inf if s > 0 else -np.inf), dtype=f32) if s else x0
+                for _ in range(abs(s) - 1):
+                    xc = np.nextafter(xc, f32(np.inf if s > 0 else -np.inf), dtype=f32)
+                t = f32(xc - lo)
+                p = float(t) * float(inv)  # exact: 24 x 24 bits
+                if f32(p) == f32(k + 0.5) and p != k + 0.5 and lo < xc < hi and j < d:
+                    x[j] = xc
+                    j += 1
+        out[i] = x
+    return out
+
+
+@pytest.mark.parametrize("bw", (2, 4, 8))
+def test_writer_near_tie_products_vs_oracle(ds, O, bw):
+    """Codes whose fp32 product rounds onto a tie (the packed writer fuses the
+    product, its fixup pass must mirror exactly that arithmetic)."""
+    rng = np.random.default_rng(77 + bw)
+    d, rows = 128, 600
+    x = _near_tie_rows(rng, rows, d, (1 << bw) - 1)
+    tabs = {0: _Tab(0, x)}
+    sel = {0: np.arange(0, rows, 3, dtype=np.int64)}
+    ov = {bw: ds.AdaptiveConfig(1, 0.5)}  # naive ranges also at 2/4 bits
+    for kind in ("incremental", "full"):
+        plan = _Plan(kind, sel if kind == "incremental" else None, bw)
+        blob, qr, err = ds.build_shard_payload(_Snap(tabs, 1), plan, 0, 1024, ov)
+        ref, qr_ref, err_ref = O.build_shard_payload({0: (x, None)}, kind, sel, bw, [0],
+                                                     adaptive={bw: (1, 0.5)}, nthreads=8)
+        assert blob == ref
+        assert err == pytest.approx(err_ref, rel=1e-12, abs=1e-300)
+
+
 @pytest.mark.parametrize("bw", (2, 3, 4, 8))
 @pytest.mark.parametrize("d", (16, 20, 128))
 def test_writer_tie_heavy_rows_vs_oracle(ds, O, bw, d):
