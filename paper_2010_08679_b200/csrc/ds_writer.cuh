@@ -19,6 +19,9 @@
 #include "ds_greedy.cuh"
 #include "ds_host.h"
 
+#ifndef DS_M1_LEVELS
+#define DS_M1_LEVELS 0  // 1: 2/4-bit rows take the exact levels by shuffles (A/B r02: T 6.79 vs 6.64 ms, off)
+#endif
 #ifndef DS_M1_PACKED
 #define DS_M1_PACKED 1  // naive rows: codes and the tie check in packed fp32 pairs
 #endif
@@ -256,6 +259,14 @@ __device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x
     constexpr int EPL = C * 4;
     auto el = [&](int k) -> int { return CONTIG ? EPL * lig + k : Lay::elem(lig, k); };
     const double lod = (double)rq.lo;
+    // 2/4-bit rows on enough lanes: the row's 2^N exact levels f32(RN(RN(s*q)
+    // + lo)) (quant.py:114-115) computed once, two per lane, for the err_sum term
+    constexpr bool LEVELS = DS_M1_LEVELS && DS_ERR_F2F && G >= 2 && (1 << N) <= 2 * G;
+    float lv0 = 0.f, lv1 = 0.f;
+    if constexpr (LEVELS) {
+        lv0 = deq_exact(2 * lig, rq.lo, rq.s);
+        lv1 = deq_exact(2 * lig + 1, rq.lo, rq.s);
+    }
     float dev = 0.f;
     double sse = 0.0;
     uint32_t w[C];  // chunk c's 4 codes, N bits each, LSB first (quant.py:376-382)
@@ -300,13 +311,22 @@ __device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x
             const uint32_t qi = __float_as_uint(qm) & 0x3fffffu;
             const bool in = !PAD || el(k) < d;
 #if DS_ERR_F2F
-            // x - f32(RN(RN(s*q) + lo)), exact in f64 (DS_M1_ERR: how q enters
-            // f64 and how the level is rounded to f32 -- same value)
-            const double qd = DS_M1_ERR >= 1 ? code_to_f64(qi)
-                                             : (double)__fsub_rn(qm, 12582912.0f);
-            const double wv = __dadd_rn(__dmul_rn(rq.s, qd), lod);
-            const double dq = DS_M1_ERR >= 2 ? round_f32_in_f64(wv) : (double)__double2float_rn(wv);
-            const double er = __dsub_rn((double)x[k], dq);
+            double er;
+            if constexpr (LEVELS) {
+                // the level from the lane that holds it: two shuffles, a select
+                const int src = (threadIdx.x & 31 & ~(G - 1)) | (int)(qi >> 1);
+                const float la = __shfl_sync(DS_FULL_MASK, lv0, src);
+                const float lb = __shfl_sync(DS_FULL_MASK, lv1, src);
+                er = __dsub_rn((double)x[k], (double)((qi & 1u) ? lb : la));
+            } else {
+                // x - f32(RN(RN(s*q) + lo)), exact in f64 (DS_M1_ERR: how q enters
+                // f64 and how the level is rounded to f32 -- same value)
+                const double qd = DS_M1_ERR >= 1 ? code_to_f64(qi)
+                                                 : (double)__fsub_rn(qm, 12582912.0f);
+                const double wv = __dadd_rn(__dmul_rn(rq.s, qd), lod);
+                const double dq = DS_M1_ERR >= 2 ? round_f32_in_f64(wv) : (double)__double2float_rn(wv);
+                er = __dsub_rn((double)x[k], dq);
+            }
 #else
             const double er = err_fast(x[k], qi, rq.s, lod);  // engine.py:171-173
 #endif
