@@ -101,8 +101,9 @@ def parse_args():
                    help="use the first T tables (smoke/profiling only)")
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="C2",
                    help="BASELINE.json config (C2 is the metric's headline config)")
-    p.add_argument("--l2-fetch", type=int, default=64,
-                   help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default)")
+    p.add_argument("--l2-fetch", type=int, default=0,
+                   help="cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default; r01's 64 "
+                        "changed no DRAM traffic, see roofline.traffic_vs_algorithmic)")
     p.add_argument("--verify-rows", type=int, default=1_000_000,
                    help="records of the last timed step's payload re-derived by the CPU oracle "
                         "(plus every header, the whole dirty-id column, section ends and the "
@@ -695,6 +696,16 @@ def run_ours(args):
                 "achieved": phases[dom]["GB/s"], "peak": peak, "unit": "GB/s",
                 "frac": phases[dom]["GB/s"] / peak, "traffic": traffic,
                 "peak_source": peak_src}
+    if traffic:
+        # DRAM moves whole sectors: a dirty row narrower than the 128-byte
+        # granule the L2 fetches for a random row read costs that granule, so
+        # measured traffic above the algorithmic bytes is the rows' scatter,
+        # not re-reads (C2: 64-byte rows)
+        alg = phases[dom].get("bytes")  # per step = per launch
+        roofline["traffic_vs_algorithmic"] = traffic / alg if alg else None
+        roofline["traffic_note"] = (
+            "ncu dram read+write bytes per launch / algorithmic bytes per launch; rows of "
+            f"{4 * DIM} B at random addresses fetch whole L2 sectors (granule 128 B)")
     if w["adaptive"] and dom == "write":
         # the greedy search is compute-bound: SURVEY 8(d)'s op count per row,
         # 13*d*(E+1) + 2d with E = 2*steps + 1 candidate evaluations, against

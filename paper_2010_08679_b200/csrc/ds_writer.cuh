@@ -1373,6 +1373,12 @@ static writer_fn select_writer(const Cfg &c) {
     if constexpr (MODE != 2) {
         DS_W(1, 8, 4) DS_W(2, 8, 4) DS_W(4, 8, 4) DS_W(8, 8, 4) DS_W(16, 8, 4)
     }
+#if DS_EPL_GREEDY == 32
+    if constexpr (MODE == 2) {
+        DS_W(1, 8, 4) DS_W(2, 8, 4) DS_W(4, 8, 4) DS_W(8, 8, 4) DS_W(16, 8, 4)
+        DS_W(1, 32, 1) DS_W(2, 32, 1) DS_W(4, 32, 1) DS_W(8, 32, 1) DS_W(16, 32, 1)
+    }
+#endif
 #if DS_EPL_GREEDY == 8
     if constexpr (MODE == 2) {
         DS_W(2, 2, 4) DS_W(4, 2, 4) DS_W(8, 2, 4) DS_W(16, 2, 4) DS_W(32, 2, 4)
