@@ -581,11 +581,96 @@ struct Cand {
     bool has_me;
 };
 
+#ifndef DS_GREEDY_LEAN
+#define DS_GREEDY_LEAN 1  // decisions: certified fast path, exact bookkeeping behind one warp vote
+#endif
 template <int G, int C, int VEC, bool PAD>
 __device__ __forceinline__ void greedy_row(const float (&x)[C * VEC], int d, int lig, bool row_ok,
                                            float lo0, float hi0, int L, int bins, int steps,
                                            double *buf, float &out_lo, float &out_hi,
                                            unsigned &n_exact_dec, unsigned &n_exact_codes) {
+#if DS_GREEDY_LEAN
+    // the reference's decisions (take_a = me_a <= me_b, quant.py:198;
+    // improved = me_cur < best_me, :204) from certified fp32 intervals; a
+    // comparison whose intervals overlap is re-taken with exact MEs
+    // (exact_me_group), the cached exact ME of `best` reused while it stands
+    const double full = __dsub_rn((double)hi0, (double)lo0);
+    const double step = __ddiv_rn(full, (double)bins);
+    float best_lo = lo0, best_hi = hi0, best_S, best_B;
+    double best_me = 0.0;
+    bool best_has_me = false;
+    eval_fast<G, C, VEC, PAD>(x, d, lig, lo0, hi0, L, best_S, best_B);
+    double cur_lo = (double)lo0, cur_hi = (double)hi0;
+    bool active = row_ok && step > 0.0;
+    for (int it = 0; it < steps; it++) {
+        active = active && (__dsub_rn(__dsub_rn(cur_hi, cur_lo), step) > 0.0);
+        if (!__any_sync(DS_FULL_MASK, active)) break;
+        const float a_lo = __double2float_rn(__dadd_rn(cur_lo, step)), a_hi = __double2float_rn(cur_hi);
+        const float b_lo = __double2float_rn(cur_lo), b_hi = __double2float_rn(__dsub_rn(cur_hi, step));
+        float SA, BA, SB, BB;
+        eval_fast2<G, C, VEC, PAD>(x, d, lig, a_lo, a_hi, b_lo, b_hi, L, SA, BA, SB, BB);
+        const bool ta_yes = SA + BA < SB - BB, ta_no = SA - BA > SB + BB;
+        bool take_a = !ta_no;
+        float Sc = take_a ? SA : SB, Bc = take_a ? BA : BB;
+        const bool imp_yes = Sc + Bc < best_S - best_B, imp_no = Sc - Bc > best_S + best_B;
+        bool improved = imp_yes;
+        double me_c = 0.0;
+        bool c_has = false;
+        if (__any_sync(DS_FULL_MASK, active && !((ta_yes || ta_no) && (imp_yes || imp_no)))) {
+            const bool need_t = active && !(ta_yes || ta_no);
+            if (__any_sync(DS_FULL_MASK, need_t)) {
+                const double ma = exact_me_group<G, C, VEC>(x, d, lig, a_lo, a_hi, L, need_t, buf, n_exact_codes);
+                const double mb = exact_me_group<G, C, VEC>(x, d, lig, b_lo, b_hi, L, need_t, buf, n_exact_codes);
+                if (need_t) {
+                    take_a = ma <= mb;
+                    me_c = take_a ? ma : mb;
+                    c_has = true;
+                    if (lig == 0) n_exact_dec++;
+                }
+            }
+            Sc = take_a ? SA : SB;
+            Bc = take_a ? BA : BB;
+            const bool iy = Sc + Bc < best_S - best_B, in_ = Sc - Bc > best_S + best_B;
+            improved = iy;
+            const bool undecided = active && !(iy || in_);
+            const float c_lo = take_a ? a_lo : b_lo, c_hi = take_a ? a_hi : b_hi;
+            const bool need_c = undecided && !c_has, need_b = undecided && !best_has_me;
+            if (__any_sync(DS_FULL_MASK, need_c)) {
+                const double m = exact_me_group<G, C, VEC>(x, d, lig, c_lo, c_hi, L, need_c, buf, n_exact_codes);
+                if (need_c) {
+                    me_c = m;
+                    c_has = true;
+                }
+            }
+            if (__any_sync(DS_FULL_MASK, need_b)) {
+                const double m = exact_me_group<G, C, VEC>(x, d, lig, best_lo, best_hi, L, need_b, buf, n_exact_codes);
+                if (need_b) {
+                    best_me = m;
+                    best_has_me = true;
+                }
+            }
+            if (undecided) {
+                improved = me_c < best_me;
+                if (lig == 0) n_exact_dec++;
+            }
+        }
+        if (active) {
+            if (take_a) cur_lo = __dadd_rn(cur_lo, step);
+            else cur_hi = __dsub_rn(cur_hi, step);
+            if (improved) {
+                best_lo = take_a ? a_lo : b_lo;
+                best_hi = take_a ? a_hi : b_hi;
+                best_S = Sc;
+                best_B = Bc;
+                best_me = me_c;
+                best_has_me = c_has;
+            }
+        }
+    }
+    out_lo = best_lo;
+    out_hi = best_hi;
+#else
+
     double full = __dsub_rn((double)hi0, (double)lo0);
     double step = __ddiv_rn(full, (double)bins);
     Cand best;
@@ -663,6 +748,7 @@ __device__ __forceinline__ void greedy_row(const float (&x)[C * VEC], int d, int
     }
     out_lo = best.lo;
     out_hi = best.hi;
+#endif
 }
 
 }  // namespace ds
