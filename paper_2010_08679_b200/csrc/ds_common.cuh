@@ -521,8 +521,20 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
             if (PAD && !(Lay::elem(lig, k) < d)) e = pk2(0.f, 0.f);
             sse = fma2(e, e, sse);
         }
+        // group sums of both candidates in one packed add per level (the
+        // scalar path's order: each value plus its xor partner)
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            float a, b;
+            up2(sse, a, b);
+            sse = add2(sse, pk2(__shfl_xor_sync(DS_FULL_MASK, a, o, G), __shfl_xor_sync(DS_FULL_MASK, b, o, G)));
+        }
         up2(sse, sseA, sseB);
     }
+    // a code tie anywhere in the group: one ballot per candidate
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const bool tieA = (__ballot_sync(DS_FULL_MASK, rmA > 0.5f - 10.f * kU * (float)L) & gmask) != 0u;
+    const bool tieB = (__ballot_sync(DS_FULL_MASK, rmB > 0.5f - 10.f * kU * (float)L) & gmask) != 0u;
 #else
 #pragma unroll
     for (int k = 0; k < EPL; k++) {
@@ -547,7 +559,6 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
         sseA = __fmaf_rn(eA, eA, sseA);
         sseB = __fmaf_rn(eB, eB, sseB);
     }
-#endif
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
         sseA += __shfl_xor_sync(DS_FULL_MASK, sseA, o, G);
@@ -555,20 +566,22 @@ __device__ __forceinline__ void eval_fast2(const float (&x)[C * VEC], int d, int
         rmA = fmaxf(rmA, __shfl_xor_sync(DS_FULL_MASK, rmA, o, G));
         rmB = fmaxf(rmB, __shfl_xor_sync(DS_FULL_MASK, rmB, o, G));
     }
+    const bool tieA = rmA > 0.5f - 10.f * kU * (float)L, tieB = rmB > 0.5f - 10.f * kU * (float)L;
+#endif
     SA = sseA;
     SB = sseB;
     const float fd = (float)d;
     const float epsw = 10.f * kU * (float)L;  // |v_fast - v_ref|
-    auto bound = [&](float S, float M, float s32, float rmax, bool ok) -> float {
+    auto bound = [&](float S, float M, float s32, bool tie, bool ok) -> float {
         if (!ok) return INFINITY;
         const float delta = 16.f * kU * M + 1e-44f;  // |deq_fast - deq_ref|
         float b = 2.f * delta * sqrtf(fd * S) + 2.f * fd * delta * delta +
                   (float)(EPL + log2i<G>() + 4) * kU * S;
-        if (rmax > 0.5f - epsw) b += fd * 4.f * s32 * (epsw * s32 + 2.f * delta);  // code ties
+        if (tie) b += fd * 4.f * s32 * (epsw * s32 + 2.f * delta);  // code ties
         return 1.5f * b + 1e-37f;
     };
-    BA = bound(SA, MA, sA, rmA, okA);
-    BB = bound(SB, MB, sB, rmB, okB);
+    BA = bound(SA, MA, sA, tieA, okA);
+    BB = bound(SB, MB, sB, tieB, okB);
 }
 
 // ---------------------------------------------------------------------------
