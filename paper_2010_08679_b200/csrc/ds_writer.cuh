@@ -19,6 +19,12 @@
 #include "ds_greedy.cuh"
 #include "ds_host.h"
 
+#ifndef DS_ERR_DEFER
+// 1: code_row_m1 leaves its row's sum of squares to the warp writer, which
+// takes each tile row's root on its own lane (one root per 32 rows instead of
+// one per group per chunk); only the G > 1 warp writer calls code_row_m1
+#define DS_ERR_DEFER 1
+#endif
 #ifndef DS_M1_LEVELS
 #define DS_M1_LEVELS 0  // 1: 2/4-bit rows take the exact levels by shuffles (A/B r02: T 6.79 vs 6.64 ms, off)
 #endif
@@ -242,6 +248,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // per-thread accumulators of the writer
 struct WAcc {
     double err = 0.0;  // sum of row L2 errors (engine.py:171-173)
+    double row_sse = 0.0;  // DS_ERR_DEFER: the last code_row_m1 row's sum of squares (group-reduced)
     unsigned n_exact_dec = 0, n_exact_codes = 0, n_rows = 0;
     bool bad_data = false, bad_ids = false;
 };
@@ -339,8 +346,9 @@ __device__ __forceinline__ bool code_row_m1(const WriterArgs &a, const float (&x
     const bool fix = row_ok && (rq.mode == 2 || dev > 0.5f - rq.eps);
     if (rq.mode == 2 || !row_ok) sse = 0.0;  // mode 2: the fixup adds the exact error
     sse = grp_sumd<G>(sse);
+    if (DS_ERR_DEFER) acc.row_sse = sse;  // the warp takes the root once per tile row (one lane each)
     if (row_ok && lig == 0) {
-        acc.err += DS_ERR_F2F ? (sse > 0.0 ? sse * rsqrt(sse) : 0.0) : row_err(sse);
+        if (!DS_ERR_DEFER) acc.err += DS_ERR_F2F ? (sse > 0.0 ? sse * rsqrt(sse) : 0.0) : row_err(sse);
         acc.n_rows++;
         if (al8)
             *reinterpret_cast<uint2 *>(rec + a.par_off) = make_uint2(__float_as_uint(rq.lo), __float_as_uint(rq.hi));
@@ -1161,6 +1169,7 @@ __global__ void __launch_bounds__(MODE == 2 ? DS_WT_GREEDY : DS_WT_WARP,
             const TI far = tinfo(j + 2);  // ids two tiles ahead (plain loads, consumed a tile later)
             const ds_table_desc &td = a.t[cur.t];
             bool row_fix = false;  // lane r: record r of the tile goes to the fixup pass
+            double tile_sse = 0.0;  // lane r: record r's sum of squares (DS_ERR_DEFER)
 #pragma unroll 1
             for (int sub = 0; sub < NCH; sub++) {
                 // keep NS-1 chunks in flight
@@ -1204,14 +1213,23 @@ __global__ void __launch_bounds__(MODE == 2 ? DS_WT_GREEDY : DS_WT_WARP,
                     if (__any_sync(DS_FULL_MASK, fix))
                         fix_rows_inline<G, C, VEC, PAD, VEC == 4 && G == 1>(a, x, lig, d, fix, stage + r * a.rec,
                                                                             codes + slot * d, acc);
-                } else if (MODE == 1) {  // record r's flag to lane r
-                    const bool f = __shfl_sync(DS_FULL_MASK, fix, ((lane - sub * RPC) & (RPC - 1)) * G);
-                    if (lane >= sub * RPC && lane < (sub + 1) * RPC) row_fix |= f;
+                } else if (MODE == 1) {  // record r's flag (and sum of squares) to lane r
+                    const int from = ((lane - sub * RPC) & (RPC - 1)) * G;
+                    const bool mine = lane >= sub * RPC && lane < (sub + 1) * RPC;
+                    const bool f = __shfl_sync(DS_FULL_MASK, fix, from);
+                    if (mine) row_fix |= f;
+                    if (DS_ERR_DEFER) {
+                        const double rs = __shfl_sync(DS_FULL_MASK, acc.row_sse, from);
+                        if (mine) tile_sse = rs;
+                        acc.row_sse = 0.0;
+                    }
                 }
                 __syncwarp();  // every lane is done with ring stage cst before it is refilled
                 cst = cst + 1 == NS ? 0 : cst + 1;
             }
             irel--;  // the next tile becomes the current one
+            if (MODE == 1 && !FIXIN && DS_ERR_DEFER)  // the tile's row errors, 32 roots at once
+                acc.err += DS_ERR_F2F ? (tile_sse > 0.0 ? tile_sse * rsqrt(tile_sse) : 0.0) : row_err(tile_sse);
             if (MODE == 1 && !FIXIN) {
                 const unsigned fm = __ballot_sync(DS_FULL_MASK, row_fix);
                 if (lane == 0) a.fix_mask[tbeg + (int64_t)j * tstep] = fm;
