@@ -193,6 +193,9 @@ __device__ __forceinline__ double row_err(double sse) {
 // ---------------------------------------------------------------------------
 // final codes of a row with fixed (lo, hi): fp32 guard band + exact fallback
 // ---------------------------------------------------------------------------
+#ifndef DS_RCP_RN
+#define DS_RCP_RN 0
+#endif
 struct RowQ {
     float lo, hi, inv, eps;
     double s;
@@ -228,10 +231,17 @@ __device__ __forceinline__ RowQ make_rowq(float lo, float hi, int L, double y = 
         r.mode = 2;
     } else {
         r.mode = 0;
-        // inv = L/rng via a correctly rounded reciprocal and one product:
-        // rel. error <= 3u (rng, rcp, mul); with c-lo and v = t*inv that is
-        // |v_fast - v_ref| <= 5u*L, covered by the 8u*L guard band
+        // inv = L/rng via the hardware reciprocal (MUFU.RCP, rel. error <=
+        // 2^-23 = 2u) and one product: rel. error <= 4u (rng, rcp, mul); with
+        // c-lo and v = t*inv that is |v_fast - v_ref| <= 6u*L, covered by the
+        // 8u*L guard band (DS_RCP_RN=1: the correctly rounded reciprocal, 5u*L)
+#if DS_RCP_RN
         r.inv = __fmul_rn(__frcp_rn(rng), (float)L);
+#else
+        float rc;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(rng));
+        r.inv = __fmul_rn(rc, (float)L);
+#endif
         r.eps = 8.f * kU * (float)L;
     }
     return r;
